@@ -1,0 +1,618 @@
+/*
+ * isf_oracle.c -- CPU ORACLE (test infrastructure, never shipped).  See isf_oracle.h
+ * for scope, citations and the parity-pinning status.
+ *
+ * Build: oracle/Makefile (gcc -O2 -fopenmp -ffp-contract=off).  -ffp-contract=off
+ * matters: every fused multiply-add in the pinned evaluation order is an explicit
+ * fma() call, every other product/sum is a separately rounded operation, exactly
+ * as the CUDA kernels use __fma_rn / __dmul_rn / __dadd_rn.
+ */
+#include "isf_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ISO_MAX_LX 16
+#define ERR_SHAPE 13   /* 1 + ErrorCode::ShapeMismatch   (proj/include/isf/core/errors.hpp:21) */
+#define ERR_INVALID 21 /* 1 + ErrorCode::InvalidArgument (proj/include/isf/core/errors.hpp:36) */
+
+/* ------------------------------------------------------------------------- */
+/* GLL nodes / weights / Legendre matrices.               */
+/* Nodes: +-1 and the roots of P'_N (N = lx-1), Newton in long double on       */
+/* x P_N - P_{N-1} = 0 ... mirrored exactly x_{N-i} = -x_i.                    */
+/* ------------------------------------------------------------------------- */
+static void legendre_all(int N, long double x, long double* P /* N+1 */) {
+    P[0] = 1.0L;
+    if (N >= 1) P[1] = x;
+    for (int k = 2; k <= N; ++k)
+        P[k] = ((long double)(2 * k - 1) * x * P[k - 1] - (long double)(k - 1) * P[k - 2]) /
+               (long double)k;
+}
+
+static void gll_ld(int lx, long double* x, long double* w) {
+    const int N = lx - 1;
+    long double P[ISO_MAX_LX + 1];
+    for (int i = 0; i <= N; ++i) {
+        /* Chebyshev-Gauss-Lobatto initial guess, ascending order */
+        long double xi = -cosl(3.14159265358979323846264338327950288L * (long double)i / (long double)N);
+        for (int it = 0; it < 100; ++it) {
+            legendre_all(N, xi, P);
+            long double dx = (xi * P[N] - P[N - 1]) / ((long double)(N + 1) * P[N]);
+            xi -= dx;
+            if (fabsl(dx) < 1e-30L) break;
+        }
+        x[i] = xi;
+    }
+    x[0] = -1.0L;
+    x[N] = 1.0L;
+    for (int i = 0; i < lx / 2; ++i) x[N - i] = -x[i];
+    if (lx % 2) x[lx / 2] = 0.0L;
+    for (int i = 0; i <= N; ++i) {
+        legendre_all(N, x[i], P);
+        w[i] = 2.0L / ((long double)N * (long double)(N + 1) * P[N] * P[N]);
+    }
+    for (int i = 0; i < lx / 2; ++i) w[N - i] = w[i];
+}
+
+int iso_gll(int lx, double* x, double* w) {
+    if (lx < 2 || lx > ISO_MAX_LX) return ERR_INVALID;
+    long double xl[ISO_MAX_LX], wl[ISO_MAX_LX];
+    gll_ld(lx, xl, wl);
+    for (int i = 0; i < lx; ++i) {
+        x[i] = (double)xl[i];
+        w[i] = (double)wl[i];
+    }
+    return 0;
+}
+
+/* F[k][i] = w_i L_k(x_i) / sqrt(gamma_k);  B[i][k] = L_k(x_i) / sqrt(gamma_k)
+ * gamma_k = 2/(2k+1) (k < N), gamma_N = 2/N (discrete GLL norm of L_N).
+ * Computed for i <= N/2 and mirrored with (-1)^k so the parity identity holds bitwise;
+ * for odd lx the middle node is 0 and the odd-k entries there are exactly 0. */
+int iso_matrices(int lx, double* F, double* B) {
+    if (lx < 2 || lx > ISO_MAX_LX) return ERR_INVALID;
+    const int N = lx - 1;
+    long double x[ISO_MAX_LX], w[ISO_MAX_LX], P[ISO_MAX_LX + 1];
+    gll_ld(lx, x, w);
+    for (int i = 0; i < (lx + 1) / 2; ++i) {
+        legendre_all(N, x[i], P);
+        for (int k = 0; k < lx; ++k) {
+            long double g = (k < N) ? 2.0L / (long double)(2 * k + 1) : 2.0L / (long double)N;
+            long double rs = 1.0L / sqrtl(g);
+            double f = (double)(w[i] * P[k] * rs);
+            double b = (double)(P[k] * rs);
+            if ((lx % 2) && i == lx / 2 && (k % 2)) { f = 0.0; b = 0.0; }
+            F[k * lx + i] = f;
+            B[i * lx + k] = b;
+            if (i != N - i) {
+                F[k * lx + (N - i)] = (k % 2) ? -f : f;
+                B[(N - i) * lx + k] = (k % 2) ? -b : b;
+            }
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Pinned 1-D line transforms.                                */
+/* ------------------------------------------------------------------------- */
+static inline void fwd_line(int n, const double* F, const double* u, int su, double* a, int sa) {
+    const int h = n / 2;
+    double s[ISO_MAX_LX / 2], d[ISO_MAX_LX / 2];
+    for (int i = 0; i < h; ++i) {
+        double x0 = u[i * su], x1 = u[(n - 1 - i) * su];
+        s[i] = x0 + x1;
+        d[i] = x0 - x1;
+    }
+    const double m = (n & 1) ? u[h * su] : 0.0;
+    for (int k = 0; k < n; ++k) {
+        const double* Fk = F + k * n;
+        const double* v = (k & 1) ? d : s;
+        double acc = Fk[0] * v[0];
+        for (int i = 1; i < h; ++i) acc = fma(Fk[i], v[i], acc);
+        if ((n & 1) && !(k & 1)) acc = fma(Fk[h], m, acc);
+        a[k * sa] = acc;
+    }
+}
+
+static inline void inv_line(int n, const double* B, const double* a, int sa, double* u, int su) {
+    const int h = n / 2;
+    double out[ISO_MAX_LX];
+    for (int i = 0; i < h; ++i) {
+        const double* Bi = B + i * n;
+        double E = Bi[0] * a[0];
+        for (int k = 2; k < n; k += 2) E = fma(Bi[k], a[k * sa], E);
+        double O = Bi[1] * a[1 * sa];
+        for (int k = 3; k < n; k += 2) O = fma(Bi[k], a[k * sa], O);
+        out[i] = E + O;
+        out[n - 1 - i] = E - O;
+    }
+    if (n & 1) {
+        const double* Bh = B + h * n;
+        double E = Bh[0] * a[0];
+        for (int k = 2; k < n; k += 2) E = fma(Bh[k], a[k * sa], E);
+        out[h] = E;
+    }
+    for (int i = 0; i < n; ++i) u[i * su] = out[i];
+}
+
+/* forward: z sweep, then y, then x (in place on a scratch copy) */
+void iso_fwd_block(int lx, const double* F, const double* u, double* a) {
+    const int n = lx, n2 = lx * lx, n3 = n2 * lx;
+    double t[ISO_MAX_LX];
+    memcpy(a, u, sizeof(double) * (size_t)n3);
+    for (int y = 0; y < n; ++y)
+        for (int x = 0; x < n; ++x) {
+            fwd_line(n, F, a + y * n + x, n2, t, 1);
+            for (int k = 0; k < n; ++k) a[k * n2 + y * n + x] = t[k];
+        }
+    for (int z = 0; z < n; ++z)
+        for (int x = 0; x < n; ++x) {
+            fwd_line(n, F, a + z * n2 + x, n, t, 1);
+            for (int k = 0; k < n; ++k) a[z * n2 + k * n + x] = t[k];
+        }
+    for (int z = 0; z < n; ++z)
+        for (int y = 0; y < n; ++y) {
+            fwd_line(n, F, a + z * n2 + y * n, 1, t, 1);
+            for (int k = 0; k < n; ++k) a[z * n2 + y * n + k] = t[k];
+        }
+}
+
+/* inverse: x sweep, then y, then z */
+void iso_inv_block(int lx, const double* B, const double* a, double* u) {
+    const int n = lx, n2 = lx * lx, n3 = n2 * lx;
+    double t[ISO_MAX_LX];
+    memcpy(u, a, sizeof(double) * (size_t)n3);
+    for (int z = 0; z < n; ++z)
+        for (int y = 0; y < n; ++y) {
+            inv_line(n, B, u + z * n2 + y * n, 1, t, 1);
+            for (int k = 0; k < n; ++k) u[z * n2 + y * n + k] = t[k];
+        }
+    for (int z = 0; z < n; ++z)
+        for (int x = 0; x < n; ++x) {
+            inv_line(n, B, u + z * n2 + x, n, t, 1);
+            for (int k = 0; k < n; ++k) u[z * n2 + k * n + x] = t[k];
+        }
+    for (int y = 0; y < n; ++y)
+        for (int x = 0; x < n; ++x) {
+            inv_line(n, B, u + y * n + x, n2, t, 1);
+            for (int k = 0; k < n; ++k) u[k * n2 + y * n + x] = t[k];
+        }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Pinned truncation rule, SPEC.md:225 made exact:            */
+/*   K      = min(25, floor((63 - ceil(log2 lx^3)) / 2))  (e_j < 2^50 < 2^52)   */
+/*   s      = frexp exponent of max|a|   (2^(s-1) <= max|a| < 2^s)            */
+/*   a''_j  = |a_j| * 2^(K-s)            (exact whenever the result is >= 1)  */
+/*   e_j    = fl(a''_j * a''_j)  in [0, 2^50)                                 */
+/*   lo_j   = floor(e_j), hi_j = ceil(e_j)           (integers, u64)          */
+/*   T      = sum lo_j,  q = floor(fl(eps*eps) * 2^64),  thr = floor(T*q/2^64) */
+/*   discard order: |a| ascending, ties by index descending (= sort by |c|    */
+/*   descending, index ascending, read from the end)                         */
+/*   D      = longest prefix of the discard order with sum hi <= thr          */
+/*   kept   = complement of D; an all-zero block keeps nothing.               */
+/* Integer sums are exact and order independent, so any correct GPU          */
+/* selection reproduces the mask bit for bit.                                 */
+/* ------------------------------------------------------------------------- */
+static int ceil_log2_u32(uint32_t v) {
+    int r = 0;
+    while ((1u << r) < v) ++r;
+    return r;
+}
+
+static int energy_K(int lx) {
+    int K = (63 - ceil_log2_u32((uint32_t)(lx * lx * lx))) / 2;
+    return K < 25 ? K : 25;
+}
+
+typedef struct {
+    uint64_t key; /* |a| bits */
+    int idx;
+} sel_item;
+
+static int cmp_discard_order(const void* pa, const void* pb) {
+    const sel_item* a = (const sel_item*)pa;
+    const sel_item* b = (const sel_item*)pb;
+    if (a->key != b->key) return a->key < b->key ? -1 : 1;
+    return b->idx - a->idx; /* larger index discarded first */
+}
+
+static uint64_t mulhi64(uint64_t a, uint64_t b) {
+    return (uint64_t)(((unsigned __int128)a * (unsigned __int128)b) >> 64);
+}
+
+static uint64_t eps_q(double max_error) {
+    double e2 = max_error * max_error;
+    return (uint64_t)ldexp(e2, 64); /* e2 < 1 => < 2^64; truncation = floor */
+}
+
+static uint32_t select_impl(int lx, const double* a, double max_error, double rel, uint64_t* mask,
+                            uint64_t* lo_total, uint64_t* lo_disc, int* scale_exp, int* nonfinite) {
+    const int n3 = lx * lx * lx;
+    const int W = (n3 + 63) / 64;
+    for (int w = 0; w < W; ++w) mask[w] = 0;
+    uint64_t maxbits = 0;
+    for (int j = 0; j < n3; ++j) {
+        uint64_t b;
+        memcpy(&b, &a[j], 8);
+        b &= 0x7fffffffffffffffull;
+        if (b > maxbits) maxbits = b;
+    }
+    if (lo_total) *lo_total = 0;
+    if (lo_disc) *lo_disc = 0;
+    if (scale_exp) *scale_exp = 0;
+    if (nonfinite) *nonfinite = 0;
+    if (maxbits >= 0x7ff0000000000000ull) {
+        if (nonfinite) *nonfinite = 1;
+        return 0;
+    }
+    if (maxbits == 0) return 0; /* all-zero block keeps 0 coefficients */
+    double amax;
+    memcpy(&amax, &maxbits, 8);
+    int s;
+    (void)frexp(amax, &s);
+    const int K = energy_K(lx);
+    const int k = K - s;
+    static __thread sel_item items[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+    static __thread uint64_t hi[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+    static __thread uint64_t lo[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+    uint64_t T = 0;
+    for (int j = 0; j < n3; ++j) {
+        double as = ldexp(fabs(a[j]), k);
+        double e = as * as;
+        double fl = floor(e), ce = ceil(e);
+        lo[j] = (uint64_t)fl;
+        hi[j] = (uint64_t)ce;
+        T += lo[j];
+        uint64_t b;
+        memcpy(&b, &a[j], 8);
+        items[j].key = b & 0x7fffffffffffffffull;
+        items[j].idx = j;
+    }
+    uint64_t thr = mulhi64(T, eps_q(max_error));
+    if (rel != 0.0) {
+        long double t = (long double)thr * (1.0L + (long double)rel);
+        thr = t <= 0.0L ? 0 : (t >= 18446744073709551615.0L ? ~0ull : (uint64_t)t);
+    }
+    qsort(items, (size_t)n3, sizeof(sel_item), cmp_discard_order);
+    uint64_t acc = 0;
+    int m = 0;
+    while (m < n3 && acc + hi[items[m].idx] <= thr) {
+        acc += hi[items[m].idx];
+        ++m;
+    }
+    for (int p = m; p < n3; ++p) {
+        int j = items[p].idx;
+        mask[j >> 6] |= 1ull << (j & 63);
+    }
+    if (lo_total) *lo_total = T;
+    if (lo_disc) *lo_disc = acc; /* hi-sum of the discarded set (upper bound) */
+    if (scale_exp) *scale_exp = -2 * k;
+    return (uint32_t)(n3 - m);
+}
+
+uint32_t iso_select_block(int lx, const double* a, double max_error, uint64_t* mask,
+                          uint64_t* lo_total, uint64_t* lo_disc, int* scale_exp, int* nonfinite) {
+    return select_impl(lx, a, max_error, 0.0, mask, lo_total, lo_disc, scale_exp, nonfinite);
+}
+
+uint32_t iso_select_block_perturbed(int lx, const double* a, double max_error, double rel,
+                                    uint64_t* mask) {
+    return select_impl(lx, a, max_error, rel, mask, NULL, NULL, NULL, NULL);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Stream format, little-endian:                              */
+/*   counts u32[B] | pad to 8 | masks u64[B][W] | values f64[sum counts]      */
+/* Block b = element*comps + comp; values in ascending coefficient index.     */
+/* ------------------------------------------------------------------------- */
+uint64_t iso_stream_header_bytes(int lx, uint64_t nblocks) {
+    const uint64_t W = ((uint64_t)lx * lx * lx + 63) / 64;
+    return ((4 * nblocks + 7) & ~7ull) + 8 * W * nblocks;
+}
+
+uint64_t iso_stream_capacity(int lx, uint64_t nblocks) {
+    return iso_stream_header_bytes(lx, nblocks) + 8ull * lx * lx * lx * nblocks;
+}
+
+static void gather_block(int n3, int comps, const double* field, uint64_t e, int c, double* out) {
+    const double* base = field + e * (uint64_t)n3 * comps + c;
+    for (int p = 0; p < n3; ++p) out[p] = base[(uint64_t)p * comps];
+}
+
+static int omp_threads(int nthreads) {
+#ifdef _OPENMP
+    return nthreads > 0 ? nthreads : omp_get_max_threads();
+#else
+    (void)nthreads;
+    return 1;
+#endif
+}
+
+int iso_compress(int lx, int comps, uint64_t n_elements, const double* field, double max_error,
+                 uint8_t* stream, uint64_t cap, uint64_t* stream_bytes, iso_stats* st, int nthreads) {
+    if (lx < 2 || lx > ISO_MAX_LX || (comps != 1 && comps != 3)) return ERR_INVALID;
+    if (!(max_error > 0.0 && max_error < 1.0)) return ERR_INVALID;
+    const int n3 = lx * lx * lx, W = (n3 + 63) / 64;
+    const uint64_t B = n_elements * (uint64_t)comps;
+    const uint64_t hdr = iso_stream_header_bytes(lx, B);
+    if (cap < hdr) return ERR_INVALID;
+    double F[ISO_MAX_LX * ISO_MAX_LX], Bm[ISO_MAX_LX * ISO_MAX_LX];
+    iso_matrices(lx, F, Bm);
+    uint32_t* counts = (uint32_t*)stream;
+    uint64_t* masks = (uint64_t*)(stream + ((4 * B + 7) & ~7ull));
+    if (B & 1) counts[B] = 0; /* pad */
+    const int nt = omp_threads(nthreads);
+    double** tbuf = (double**)calloc((size_t)nt, sizeof(double*));
+    uint64_t* tcount = (uint64_t*)calloc((size_t)nt, sizeof(uint64_t));
+    double* tdisc = (double*)calloc((size_t)nt, sizeof(double));
+    double* ttot = (double*)calloc((size_t)nt, sizeof(double));
+    int* tbad = (int*)calloc((size_t)nt, sizeof(int));
+#pragma omp parallel num_threads(nt)
+    {
+#ifdef _OPENMP
+        const int t = omp_get_thread_num();
+#else
+        const int t = 0;
+#endif
+        const uint64_t b0 = B * (uint64_t)t / (uint64_t)nt, b1 = B * (uint64_t)(t + 1) / (uint64_t)nt;
+        size_t capv = 1024, nv = 0;
+        double* vals = (double*)malloc(capv * sizeof(double));
+        double u[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX], a[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+        double disc = 0.0, tot = 0.0;
+        for (uint64_t b = b0; b < b1; ++b) {
+            gather_block(n3, comps, field, b / comps, (int)(b % comps), u);
+            iso_fwd_block(lx, F, u, a);
+            uint64_t* mk = masks + b * W;
+            uint64_t lt, ld;
+            int se, nf;
+            uint32_t kept = iso_select_block(lx, a, max_error, mk, &lt, &ld, &se, &nf);
+            if (nf) tbad[t] = 1;
+            counts[b] = kept;
+            tot += ldexp((double)lt, se);
+            disc += ldexp((double)ld, se);
+            if (nv + kept > capv) {
+                while (nv + kept > capv) capv *= 2;
+                vals = (double*)realloc(vals, capv * sizeof(double));
+            }
+            for (int j = 0; j < n3; ++j)
+                if (mk[j >> 6] >> (j & 63) & 1) vals[nv++] = a[j];
+        }
+        tbuf[t] = vals;
+        tcount[t] = nv;
+        tdisc[t] = disc;
+        ttot[t] = tot;
+    }
+    int rc = 0;
+    uint64_t total = 0;
+    for (int t = 0; t < nt; ++t) total += tcount[t];
+    const uint64_t bytes = hdr + 8 * total;
+    int bad = 0;
+    for (int t = 0; t < nt; ++t) bad |= tbad[t];
+    if (bad) rc = ERR_INVALID;
+    else if (bytes > cap) rc = ERR_INVALID;
+    else {
+        uint64_t off = 0;
+        for (int t = 0; t < nt; ++t) {
+            memcpy(stream + hdr + 8 * off, tbuf[t], 8 * tcount[t]);
+            off += tcount[t];
+        }
+    }
+    if (st) {
+        memset(st, 0, sizeof(*st));
+        for (int t = 0; t < nt; ++t) {
+            st->disc2 += tdisc[t];
+            st->tot2 += ttot[t];
+        }
+        st->kept = total;
+        st->blocks = B;
+        st->stream_bytes = bytes;
+        st->field_bytes = B * (uint64_t)n3 * 8;
+        st->status = bad ? 1 : 0;
+    }
+    if (stream_bytes) *stream_bytes = bytes;
+    for (int t = 0; t < nt; ++t) free(tbuf[t]);
+    free(tbuf); free(tcount); free(tdisc); free(ttot); free(tbad);
+    return rc;
+}
+
+static inline int popc64(uint64_t v) { return __builtin_popcountll(v); }
+
+int iso_decompress(int lx, int comps, uint64_t n_elements, const uint8_t* stream,
+                   uint64_t stream_bytes, double* out, const double* original, iso_stats* st,
+                   int nthreads) {
+    if (lx < 2 || lx > ISO_MAX_LX || (comps != 1 && comps != 3)) return ERR_INVALID;
+    const int n3 = lx * lx * lx, W = (n3 + 63) / 64;
+    const uint64_t B = n_elements * (uint64_t)comps;
+    const uint64_t hdr = iso_stream_header_bytes(lx, B);
+    if (stream_bytes < hdr) return ERR_SHAPE;
+    const uint32_t* counts = (const uint32_t*)stream;
+    const uint64_t* masks = (const uint64_t*)(stream + ((4 * B + 7) & ~7ull));
+    const double* vals = (const double*)(stream + hdr);
+    const uint64_t lastmask = (n3 % 64) ? ((1ull << (n3 % 64)) - 1) : ~0ull;
+    uint64_t* offs = (uint64_t*)malloc((B + 1) * sizeof(uint64_t));
+    uint64_t acc = 0;
+    int shape_bad = 0;
+    for (uint64_t b = 0; b < B; ++b) {
+        offs[b] = acc;
+        uint32_t c = 0;
+        for (int w = 0; w < W; ++w) c += (uint32_t)popc64(masks[b * W + w]);
+        if (c != counts[b] || (masks[b * W + W - 1] & ~lastmask)) shape_bad = 1;
+        acc += counts[b];
+    }
+    offs[B] = acc;
+    if (shape_bad || hdr + 8 * acc != stream_bytes) {
+        free(offs);
+        if (st) { memset(st, 0, sizeof(*st)); st->status = 2; }
+        return ERR_SHAPE;
+    }
+    double F[ISO_MAX_LX * ISO_MAX_LX], Bm[ISO_MAX_LX * ISO_MAX_LX], xg[ISO_MAX_LX], wg[ISO_MAX_LX];
+    iso_matrices(lx, F, Bm);
+    iso_gll(lx, xg, wg);
+    const int nt = omp_threads(nthreads);
+    double* terr = (double*)calloc((size_t)nt * 4, sizeof(double));
+#pragma omp parallel num_threads(nt)
+    {
+#ifdef _OPENMP
+        const int t = omp_get_thread_num();
+#else
+        const int t = 0;
+#endif
+        const uint64_t b0 = B * (uint64_t)t / (uint64_t)nt, b1 = B * (uint64_t)(t + 1) / (uint64_t)nt;
+        double a[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX], u[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+        double e2 = 0, n2 = 0, einf = 0, uinf = 0;
+        for (uint64_t b = b0; b < b1; ++b) {
+            uint64_t o = offs[b];
+            for (int j = 0; j < n3; ++j)
+                a[j] = (masks[b * W + (j >> 6)] >> (j & 63) & 1) ? vals[o++] : 0.0;
+            iso_inv_block(lx, Bm, a, u);
+            const uint64_t e = b / comps;
+            const int c = (int)(b % comps);
+            double* dst = out + e * (uint64_t)n3 * comps + c;
+            for (int p = 0; p < n3; ++p) dst[(uint64_t)p * comps] = u[p];
+            if (original) {
+                const double* src = original + e * (uint64_t)n3 * comps + c;
+                for (int z = 0; z < lx; ++z)
+                    for (int y = 0; y < lx; ++y)
+                        for (int x = 0; x < lx; ++x) {
+                            const int p = x + lx * (y + lx * z);
+                            const double w3 = (wg[x] * wg[y]) * wg[z];
+                            const double v = src[(uint64_t)p * comps];
+                            const double d = v - u[p];
+                            e2 += w3 * d * d;
+                            n2 += w3 * v * v;
+                            if (fabs(d) > einf) einf = fabs(d);
+                            if (fabs(v) > uinf) uinf = fabs(v);
+                        }
+            }
+        }
+        terr[4 * t + 0] = e2;
+        terr[4 * t + 1] = n2;
+        terr[4 * t + 2] = einf;
+        terr[4 * t + 3] = uinf;
+    }
+    if (st) {
+        memset(st, 0, sizeof(*st));
+        for (int t = 0; t < nt; ++t) {
+            st->err2 += terr[4 * t + 0];
+            st->nrm2 += terr[4 * t + 1];
+            if (terr[4 * t + 2] > st->err_inf) st->err_inf = terr[4 * t + 2];
+            if (terr[4 * t + 3] > st->u_inf) st->u_inf = terr[4 * t + 3];
+        }
+        st->kept = acc;
+        st->blocks = B;
+        st->stream_bytes = stream_bytes;
+        st->field_bytes = B * (uint64_t)n3 * 8;
+    }
+    free(terr);
+    free(offs);
+    return 0;
+}
+
+void iso_forward_field(int lx, int comps, uint64_t n_elements, const double* field, double* coeffs,
+                       int nthreads) {
+    const int n3 = lx * lx * lx;
+    const uint64_t B = n_elements * (uint64_t)comps;
+    double F[ISO_MAX_LX * ISO_MAX_LX], Bm[ISO_MAX_LX * ISO_MAX_LX];
+    iso_matrices(lx, F, Bm);
+    const int nt = omp_threads(nthreads);
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (uint64_t b = 0; b < B; ++b) {
+        double u[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+        gather_block(n3, comps, field, b / comps, (int)(b % comps), u);
+        iso_fwd_block(lx, F, u, coeffs + b * n3);
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* Synthetic inputs (TGV per SPEC.md:153-161 at t = 0, A = 1).  */
+/* ------------------------------------------------------------------------- */
+void iso_gen_tgv(int E_ax, int lx, int which, uint32_t ez0, uint32_t nz, double domain,
+                 double* out, int nthreads) {
+    double xg[ISO_MAX_LX], wg[ISO_MAX_LX];
+    iso_gll(lx, xg, wg);
+    const double h = domain / (double)E_ax;
+    const int n3 = lx * lx * lx;
+    const uint64_t nel = (uint64_t)E_ax * E_ax * nz;
+    const int nt = omp_threads(nthreads);
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (uint64_t e = 0; e < nel; ++e) {
+        const uint64_t ex = e % E_ax, ey = (e / E_ax) % E_ax, ez = e / ((uint64_t)E_ax * E_ax) + ez0;
+        double X[ISO_MAX_LX], Y[ISO_MAX_LX], Z[ISO_MAX_LX];
+        for (int i = 0; i < lx; ++i) {
+            const double r = (xg[i] + 1.0) * 0.5 * h;
+            X[i] = (double)ex * h + r;
+            Y[i] = (double)ey * h + r;
+            Z[i] = (double)ez * h + r;
+        }
+        double* o = out + e * n3;
+        for (int pz = 0; pz < lx; ++pz)
+            for (int py = 0; py < lx; ++py)
+                for (int px = 0; px < lx; ++px) {
+                    const double x = X[px], y = Y[py], z = Z[pz];
+                    double v;
+                    switch (which) {
+                        case 0: v = cos(x) * sin(y) * sin(z); break;
+                        case 1: v = -sin(x) * cos(y) * sin(z); break;
+                        case 2: v = 0.0; break;
+                        default: v = (cos(2.0 * x) + cos(2.0 * y)) * (cos(2.0 * z) + 2.0) / 16.0; break;
+                    }
+                    o[px + lx * (py + lx * pz)] = v;
+                }
+    }
+}
+
+void iso_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+void iso_spectral_amplitudes(int lx, double decay_s, double* amp) {
+    for (int m = 0; m < lx; ++m)
+        for (int l = 0; l < lx; ++l)
+            for (int k = 0; k < lx; ++k)
+                amp[k + lx * (l + lx * m)] = pow(10.0, -decay_s * sqrt((double)(k * k + l * l + m * m)));
+}
+
+void iso_gen_spectral(int lx, uint64_t block0, uint64_t nblocks, uint64_t seed, double decay_s,
+                      double* out, int nthreads) {
+    const int n3 = lx * lx * lx;
+    double F[ISO_MAX_LX * ISO_MAX_LX], Bm[ISO_MAX_LX * ISO_MAX_LX];
+    iso_matrices(lx, F, Bm);
+    double amp[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+    iso_spectral_amplitudes(lx, decay_s, amp);
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    const int nt = omp_threads(nthreads);
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (uint64_t b = 0; b < nblocks; ++b) {
+        const uint64_t g = block0 + b;
+        double a[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+        for (int j = 0; j < n3; ++j) {
+            const uint32_t ctr[4] = {(uint32_t)g, (uint32_t)(g >> 32), (uint32_t)j, 0u};
+            uint32_t r[4];
+            iso_philox4x32_10(ctr, key, r);
+            const uint64_t M = ((uint64_t)r[0] << 21) | (r[1] >> 11); /* 53 bits */
+            const double U2 = ldexp((double)(int64_t)(2 * M) - 9007199254740992.0, -53); /* 2U-1 exact */
+            a[j] = U2 * amp[j];
+        }
+        iso_inv_block(lx, Bm, a, out + b * n3);
+    }
+}

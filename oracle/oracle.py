@@ -1,0 +1,212 @@
+"""ctypes wrapper of the CPU ORACLE (oracle/isf_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / ``--impl reference`` leg.  The product package never
+imports this module.  See isf_oracle.h for what the oracle restates and its
+parity-pinning status.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_build", "libisf_oracle.so")
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("err2", ctypes.c_double), ("nrm2", ctypes.c_double),
+        ("err_inf", ctypes.c_double), ("u_inf", ctypes.c_double),
+        ("disc2", ctypes.c_double), ("tot2", ctypes.c_double),
+        ("kept", ctypes.c_uint64), ("blocks", ctypes.c_uint64),
+        ("stream_bytes", ctypes.c_uint64), ("field_bytes", ctypes.c_uint64),
+        ("status", ctypes.c_uint64), ("reserved", ctypes.c_uint64),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB_PATH) or (
+        os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "isf_oracle.c"))
+    ):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = ctypes.CDLL(_LIB_PATH)
+        P = ctypes.c_void_p
+        u64, i32, f64 = ctypes.c_uint64, ctypes.c_int, ctypes.c_double
+        L.iso_gll.argtypes = [i32, P, P]
+        L.iso_matrices.argtypes = [i32, P, P]
+        L.iso_fwd_block.argtypes = [i32, P, P, P]
+        L.iso_inv_block.argtypes = [i32, P, P, P]
+        L.iso_select_block.argtypes = [i32, P, f64, P, P, P, P, P]
+        L.iso_select_block.restype = ctypes.c_uint32
+        L.iso_select_block_perturbed.argtypes = [i32, P, f64, f64, P]
+        L.iso_select_block_perturbed.restype = ctypes.c_uint32
+        L.iso_stream_capacity.argtypes = [i32, u64]
+        L.iso_stream_capacity.restype = u64
+        L.iso_stream_header_bytes.argtypes = [i32, u64]
+        L.iso_stream_header_bytes.restype = u64
+        L.iso_compress.argtypes = [i32, i32, u64, P, f64, P, u64, P, P, i32]
+        L.iso_decompress.argtypes = [i32, i32, u64, P, u64, P, P, P, i32]
+        L.iso_forward_field.argtypes = [i32, i32, u64, P, P, i32]
+        L.iso_gen_tgv.argtypes = [i32, i32, i32, ctypes.c_uint32, ctypes.c_uint32, f64, P, i32]
+        L.iso_spectral_amplitudes.argtypes = [i32, f64, P]
+        L.iso_gen_spectral.argtypes = [i32, u64, u64, u64, f64, P, i32]
+        L.iso_philox4x32_10.argtypes = [P, P, P]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def gll(lx: int):
+    x = np.zeros(lx); w = np.zeros(lx)
+    rc = lib().iso_gll(lx, _p(x), _p(w))
+    if rc:
+        raise ValueError(f"iso_gll rc={rc}")
+    return x, w
+
+
+def matrices(lx: int):
+    F = np.zeros((lx, lx)); B = np.zeros((lx, lx))
+    rc = lib().iso_matrices(lx, _p(F), _p(B))
+    if rc:
+        raise ValueError(f"iso_matrices rc={rc}")
+    return F, B
+
+
+def fwd_block(lx, u):
+    F, _ = matrices(lx)
+    u = np.ascontiguousarray(u, dtype=np.float64).reshape(-1)
+    a = np.zeros_like(u)
+    lib().iso_fwd_block(lx, _p(F), _p(u), _p(a))
+    return a
+
+
+def inv_block(lx, a):
+    _, B = matrices(lx)
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    u = np.zeros_like(a)
+    lib().iso_inv_block(lx, _p(B), _p(a), _p(u))
+    return u
+
+
+def select_block(lx, a, max_error):
+    W = (lx ** 3 + 63) // 64
+    mask = np.zeros(W, dtype=np.uint64)
+    lt = ctypes.c_uint64(); ld = ctypes.c_uint64(); se = ctypes.c_int(); nf = ctypes.c_int()
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    kept = lib().iso_select_block(lx, _p(a), float(max_error), _p(mask), ctypes.byref(lt),
+                                  ctypes.byref(ld), ctypes.byref(se), ctypes.byref(nf))
+    return int(kept), mask, {"lo_total": lt.value, "lo_disc": ld.value, "scale_exp": se.value,
+                             "nonfinite": nf.value}
+
+
+def select_block_perturbed(lx, a, max_error, rel):
+    W = (lx ** 3 + 63) // 64
+    mask = np.zeros(W, dtype=np.uint64)
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    kept = lib().iso_select_block_perturbed(lx, _p(a), float(max_error), float(rel), _p(mask))
+    return int(kept), mask
+
+
+def stream_capacity(lx, nblocks):
+    return int(lib().iso_stream_capacity(lx, nblocks))
+
+
+def stream_header_bytes(lx, nblocks):
+    return int(lib().iso_stream_header_bytes(lx, nblocks))
+
+
+def compress(field: np.ndarray, lx: int, comps: int, max_error: float, nthreads: int = 0):
+    """Returns (rc, stream bytes as np.uint8 array, Stats)."""
+    field = np.ascontiguousarray(field, dtype=np.float64).reshape(-1)
+    n_el = field.size // (lx ** 3 * comps)
+    cap = stream_capacity(lx, n_el * comps)
+    buf = np.zeros(cap, dtype=np.uint8)
+    nb = ctypes.c_uint64()
+    st = Stats()
+    rc = lib().iso_compress(lx, comps, n_el, _p(field), float(max_error), _p(buf), cap,
+                            ctypes.byref(nb), ctypes.byref(st), nthreads)
+    return rc, buf[: nb.value].copy(), st
+
+
+def decompress(stream: np.ndarray, lx: int, comps: int, n_elements: int, original=None,
+               nthreads: int = 0):
+    out = np.zeros(n_elements * lx ** 3 * comps)
+    st = Stats()
+    stream = np.ascontiguousarray(stream, dtype=np.uint8)
+    orig = None
+    if original is not None:
+        orig = np.ascontiguousarray(original, dtype=np.float64).reshape(-1)
+    rc = lib().iso_decompress(lx, comps, n_elements, _p(stream), stream.size, _p(out),
+                              _p(orig) if orig is not None else None, ctypes.byref(st), nthreads)
+    return rc, out, st
+
+
+def forward_field(field, lx, comps, nthreads: int = 0):
+    field = np.ascontiguousarray(field, dtype=np.float64).reshape(-1)
+    n_el = field.size // (lx ** 3 * comps)
+    co = np.zeros(field.size)
+    lib().iso_forward_field(lx, comps, n_el, _p(field), _p(co), nthreads)
+    return co
+
+
+def gen_tgv(E_ax: int, lx: int, which: int, ez0: int = 0, nz: int | None = None,
+            domain: float = 2.0 * np.pi, nthreads: int = 0):
+    nz = E_ax if nz is None else nz
+    out = np.zeros(E_ax * E_ax * nz * lx ** 3)
+    lib().iso_gen_tgv(E_ax, lx, which, ez0, nz, float(domain), _p(out), nthreads)
+    return out
+
+
+SPECTRAL_SEED = 0x240720731
+
+
+def spectral_amplitudes(lx, decay_s=0.5):
+    amp = np.zeros(lx ** 3)
+    lib().iso_spectral_amplitudes(lx, float(decay_s), _p(amp))
+    return amp
+
+
+def gen_spectral(lx: int, nblocks: int, block0: int = 0, seed: int = SPECTRAL_SEED,
+                 decay_s: float = 0.5, nthreads: int = 0):
+    out = np.zeros(nblocks * lx ** 3)
+    lib().iso_gen_spectral(lx, block0, nblocks, seed, float(decay_s), _p(out), nthreads)
+    return out
+
+
+def philox(ctr, key):
+    c = np.asarray(ctr, dtype=np.uint32); k = np.asarray(key, dtype=np.uint32)
+    o = np.zeros(4, dtype=np.uint32)
+    lib().iso_philox4x32_10(_p(c), _p(k), _p(o))
+    return o
+
+
+# ---- stream helpers (pure numpy; same format as DESIGN.md 3.5) ----
+def parse_stream(stream: np.ndarray, lx: int, nblocks: int):
+    W = (lx ** 3 + 63) // 64
+    c_end = 4 * nblocks
+    m0 = (c_end + 7) & ~7
+    counts = stream[:c_end].view(np.uint32)
+    masks = stream[m0:m0 + 8 * W * nblocks].view(np.uint64).reshape(nblocks, W)
+    vals = stream[m0 + 8 * W * nblocks:].view(np.float64)
+    return counts, masks, vals

@@ -1,0 +1,378 @@
+// dlt_common.cuh -- device building blocks shared by the sm_100a kernels:
+// GLL operators in constant memory, the pinned even/odd line transforms,
+// lane-group primitives, decoupled look-back and the exact selection rule.
+//
+// Pinned numerics: every product/sum is an explicit __dmul_rn /
+// __dadd_rn / __fma_rn in the same order as oracle/isf_oracle.c, so the
+// coefficients, masks and streams are bit-identical to the CPU restatement of
+// SPEC.md:222-239.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace isf {
+namespace dev {
+
+constexpr int kMaxLx = 16;
+
+// Packed operator table: for each lx in [2,16], F (lx*lx, [k][i]) then B (lx*lx, [i][k]).
+// offset(lx) = 2 * sum_{m=2}^{lx-1} m^2.
+__host__ __device__ constexpr int op_offset(int lx) {
+  int o = 0;
+  for (int m = 2; m < lx; ++m) o += 2 * m * m;
+  return o;
+}
+constexpr int kOpTableSize = op_offset(kMaxLx + 1);
+__host__ __device__ constexpr int w_offset(int lx) { return (lx * (lx - 1)) / 2 - 1; }  // sum_{m=2}^{lx-1} m
+constexpr int kWTableSize = w_offset(kMaxLx + 1);
+
+// single translation unit (isf_lossy.cu) -> defined here
+__constant__ double c_ops[kOpTableSize];
+__constant__ double c_w[kWTableSize];
+__constant__ double c_x[kWTableSize];
+
+template <int LX>
+__device__ __forceinline__ double Fm(int k, int i) { return c_ops[op_offset(LX) + k * LX + i]; }
+template <int LX>
+__device__ __forceinline__ double Bm(int i, int k) { return c_ops[op_offset(LX) + LX * LX + i * LX + k]; }
+template <int LX>
+__device__ __forceinline__ double Wg(int i) { return c_w[w_offset(LX) + i]; }
+
+// ---------------------------------------------------------------------------
+// Pinned line transforms on register arrays: v[O + i*S], i = 0..LX-1.
+// forward: s_i = u_i + u_{n-1-i}, d_i = u_i - u_{n-1-i}; a_k = F[k][0]*v_0 then
+// ascending fma over the even (k even) / odd (k odd) half; middle node last.
+// ---------------------------------------------------------------------------
+template <int LX, int S, int O, int N>
+__device__ __forceinline__ void fwd_line(double (&v)[N]) {
+  constexpr int H = LX / 2;
+  double s[H], d[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const double x0 = v[O + i * S], x1 = v[O + (LX - 1 - i) * S];
+    s[i] = __dadd_rn(x0, x1);
+    d[i] = __dsub_rn(x0, x1);
+  }
+  const double m = (LX & 1) ? v[O + H * S] : 0.0;
+#pragma unroll
+  for (int k = 0; k < LX; ++k) {
+    double acc = __dmul_rn(Fm<LX>(k, 0), (k & 1) ? d[0] : s[0]);
+#pragma unroll
+    for (int i = 1; i < H; ++i) acc = __fma_rn(Fm<LX>(k, i), (k & 1) ? d[i] : s[i], acc);
+    if ((LX & 1) && !(k & 1)) acc = __fma_rn(Fm<LX>(k, H), m, acc);
+    v[O + k * S] = acc;
+  }
+}
+
+template <int LX, int S, int O, int N>
+__device__ __forceinline__ void inv_line(double (&v)[N]) {
+  constexpr int H = LX / 2;
+  double out[LX];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    double E = __dmul_rn(Bm<LX>(i, 0), v[O]);
+#pragma unroll
+    for (int k = 2; k < LX; k += 2) E = __fma_rn(Bm<LX>(i, k), v[O + k * S], E);
+    double Od = __dmul_rn(Bm<LX>(i, 1), v[O + S]);
+#pragma unroll
+    for (int k = 3; k < LX; k += 2) Od = __fma_rn(Bm<LX>(i, k), v[O + k * S], Od);
+    out[i] = __dadd_rn(E, Od);
+    out[LX - 1 - i] = __dsub_rn(E, Od);
+  }
+  if (LX & 1) {
+    double E = __dmul_rn(Bm<LX>(H, 0), v[O]);
+#pragma unroll
+    for (int k = 2; k < LX; k += 2) E = __fma_rn(Bm<LX>(H, k), v[O + k * S], E);
+    out[H] = E;
+  }
+#pragma unroll
+  for (int i = 0; i < LX; ++i) v[O + i * S] = out[i];
+}
+
+// Line transform on a pointer with runtime stride (generic kernels; same order).
+template <int LX>
+__device__ __forceinline__ void fwd_line_ptr(double* p, int stride) {
+  double v[LX];
+#pragma unroll
+  for (int i = 0; i < LX; ++i) v[i] = p[i * stride];
+  fwd_line<LX, 1, 0>(v);
+#pragma unroll
+  for (int i = 0; i < LX; ++i) p[i * stride] = v[i];
+}
+template <int LX>
+__device__ __forceinline__ void inv_line_ptr(double* p, int stride) {
+  double v[LX];
+#pragma unroll
+  for (int i = 0; i < LX; ++i) v[i] = p[i * stride];
+  inv_line<LX, 1, 0>(v);
+#pragma unroll
+  for (int i = 0; i < LX; ++i) p[i * stride] = v[i];
+}
+
+// ---------------------------------------------------------------------------
+// Energy quantisation: e = fl((|a|*2^k)^2) < 2^50,
+// lo = floor(e), hi = ceil(e) via a directed-rounding add of 2^52.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int ceil_log2(int v) {
+  int r = 0;
+  while ((1 << r) < v) ++r;
+  return r;
+}
+__host__ __device__ constexpr int energy_K(int lx) {
+  return ((63 - ceil_log2(lx * lx * lx)) / 2) < 25 ? ((63 - ceil_log2(lx * lx * lx)) / 2) : 25;
+}
+__device__ __forceinline__ uint64_t low52(double t) {
+  return (uint64_t)__double_as_longlong(t) & 0x000FFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ double pow2d(int e) {  // 2^e for e in [-1022, 1023]
+  return __longlong_as_double((long long)(e + 1023) << 52);
+}
+__device__ __forceinline__ uint64_t e_lo(double a, double f) {
+  const double t = __dmul_rn(a, f);
+  return low52(__dadd_rd(__dmul_rn(t, t), 4503599627370496.0));
+}
+__device__ __forceinline__ uint64_t e_hi(double a, double f) {
+  const double t = __dmul_rn(a, f);
+  return low52(__dadd_ru(__dmul_rn(t, t), 4503599627370496.0));
+}
+__device__ __forceinline__ uint64_t abs_bits(double a) {
+  return (uint64_t)__double_as_longlong(a) & 0x7FFFFFFFFFFFFFFFull;
+}
+
+// ---------------------------------------------------------------------------
+// Lane groups: G consecutive lanes of one warp (G | 32), xor-shuffle reductions.
+// ---------------------------------------------------------------------------
+template <int G>
+struct LaneGroup {
+  unsigned mask;  // member mask of this group
+  int rank;       // lane index inside the group
+  __device__ __forceinline__ LaneGroup() {
+    const int lane = threadIdx.x & 31;
+    rank = lane & (G - 1);
+    mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  __device__ __forceinline__ uint64_t sum(uint64_t v) const {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(mask, v, o);
+    return v;
+  }
+  __device__ __forceinline__ uint32_t sum(uint32_t v) const {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(mask, v, o);
+    return v;
+  }
+  __device__ __forceinline__ double sumd(double v) const {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(mask, v, o));
+    return v;
+  }
+  __device__ __forceinline__ uint64_t max(uint64_t v) const {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) { uint64_t t = __shfl_xor_sync(mask, v, o); v = t > v ? t : v; }
+    return v;
+  }
+  __device__ __forceinline__ uint64_t min(uint64_t v) const {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) { uint64_t t = __shfl_xor_sync(mask, v, o); v = t < v ? t : v; }
+    return v;
+  }
+  __device__ __forceinline__ uint32_t max(uint32_t v) const {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v = ::max(v, __shfl_xor_sync(mask, v, o));
+    return v;
+  }
+  __device__ __forceinline__ uint32_t min(uint32_t v) const {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v = ::min(v, __shfl_xor_sync(mask, v, o));
+    return v;
+  }
+  __device__ __forceinline__ double maxd(double v) const {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v = fmax(v, __shfl_xor_sync(mask, v, o));
+    return v;
+  }
+  // exclusive prefix sum inside the group
+  __device__ __forceinline__ uint32_t exscan(uint32_t v) const {
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      uint32_t t = __shfl_up_sync(mask, x, o, G);
+      if (rank >= o) x += t;
+    }
+    return x - v;
+  }
+  __device__ __forceinline__ uint64_t exscan(uint64_t v) const {
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      uint64_t t = __shfl_up_sync(mask, x, o, G);
+      if (rank >= o) x += t;
+    }
+    return x - v;
+  }
+  template <class T>
+  __device__ __forceinline__ T bcast(T v, int src_rank) const {
+    return __shfl_sync(mask, v, src_rank, G);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Exact selection, hard path: the candidates (keys = |a| bits, coefficient
+// indices) sit in shared memory; an MSB radix select with 64 energy-sum bins
+// finds the boundary key t* and the index cut of a tie group so that
+//   kept  <=>  key > t*  ||  (key == t* && idx < icut)
+// and the discarded set is the longest prefix of the discard order (|a| asc,
+// index desc) with sum(hi) <= R.  Group = lanes of one warp (G <= 32).
+// ---------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const uint64_t* keys,
+                                          const uint16_t* idxs, int n, uint64_t R, double f,
+                                          unsigned long long* hist, uint64_t& tstar,
+                                          uint32_t& icut, uint64_t& dsum) {
+  uint64_t klo = ~0ull, khi = 0;
+  for (int p = g.rank; p < n; p += G) {
+    const uint64_t k = keys[p];
+    klo = k < klo ? k : klo;
+    khi = k > khi ? k : khi;
+  }
+  klo = g.min(klo);
+  khi = g.max(khi);
+  dsum = 0;
+  for (;;) {
+    const uint64_t span = khi - klo;
+    if (span == 0) {
+      // tie group: every undecided candidate has key == klo
+      const uint64_t h = e_hi(__longlong_as_double((long long)klo), f);
+      uint32_t cnt = 0;
+      for (int p = g.rank; p < n; p += G) cnt += (keys[p] == klo);
+      const uint32_t gcount = g.sum(cnt);
+      uint64_t r = (h == 0) ? gcount : (R / h);
+      if (r > gcount) r = gcount;
+      dsum += r * h;
+      tstar = klo;
+      if (r == gcount) {
+        icut = 0;  // all tied discarded
+      } else if (r == 0) {
+        icut = 0xffffffffu;  // all tied kept
+      } else {
+        // keep the (gcount - r) smallest indices: icut = index of rank (gcount - r)
+        const uint32_t want = gcount - (uint32_t)r;
+        uint32_t mine = 0xffffffffu;
+        for (int p = g.rank; p < n; p += G) {
+          if (keys[p] != klo) continue;
+          const uint32_t ip = idxs[p];
+          uint32_t rank = 0;
+          for (int q = 0; q < n; ++q) rank += (keys[q] == klo && idxs[q] < ip);
+          if (rank == want) mine = ip;
+        }
+        icut = g.min(mine);
+      }
+      return;
+    }
+    const int bits = 64 - __clzll((long long)span);
+    const int shift = bits > 6 ? bits - 6 : 0;
+    for (int b = g.rank; b < 64; b += G) hist[b] = 0ull;
+    g.sync();
+    for (int p = g.rank; p < n; p += G) {
+      const uint64_t k = keys[p];
+      if (k >= klo && k <= khi)
+        atomicAdd(&hist[(k - klo) >> shift], (unsigned long long)e_hi(__longlong_as_double((long long)k), f));
+    }
+    g.sync();
+    // each lane owns 64/G consecutive bins
+    constexpr int BPL = 64 / G;
+    uint64_t loc[BPL];
+    uint64_t run = 0;
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) { run += hist[g.rank * BPL + j]; loc[j] = run; }
+    const uint64_t base = g.exscan(run);
+    const uint64_t total = g.bcast(base + run, G - 1);
+    g.sync();  // hist is reused by the next round
+    uint32_t dloc = 64;
+    uint64_t exloc = 0;
+#pragma unroll
+    for (int j = BPL - 1; j >= 0; --j) {
+      if (base + loc[j] > R) { dloc = g.rank * BPL + j; exloc = base + (j ? loc[j - 1] : 0); }
+    }
+    const uint32_t d = g.min(dloc);
+    if (d == 64) {  // everything undecided fits: discard it all
+      dsum += total;
+      tstar = khi;
+      icut = 0;
+      return;
+    }
+    const uint64_t ex = g.bcast(exloc, (int)(d / BPL));
+    R -= ex;
+    dsum += ex;
+    const uint64_t nlo = klo + ((uint64_t)d << shift);
+    const uint64_t nhi_full = nlo + ((1ull << shift) - 1);
+    const uint64_t nhi = nhi_full < khi ? nhi_full : khi;
+    uint64_t mn = ~0ull, mx = 0;
+    for (int p = g.rank; p < n; p += G) {
+      const uint64_t k = keys[p];
+      if (k >= nlo && k <= nhi) { mn = k < mn ? k : mn; mx = k > mx ? k : mx; }
+    }
+    klo = g.min(mn);
+    khi = g.max(mx);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back over warp tiles (single-pass variable-length output).
+// status word: [63:40] epoch, [39:38] flag (1 aggregate, 2 inclusive), [37:0] value
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t lb_pack(uint32_t epoch, uint32_t flag, uint64_t v) {
+  return ((uint64_t)(epoch & 0xffffffu) << 40) | ((uint64_t)flag << 38) | (v & ((1ull << 38) - 1));
+}
+
+// Called by a full warp; returns the exclusive prefix of `agg` over tiles < tile.
+__device__ __forceinline__ uint64_t warp_lookback(uint64_t* status, uint32_t tile, uint64_t agg,
+                                                  uint32_t epoch) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_relaxed(&status[0], lb_pack(epoch, 2, agg));
+    return 0;
+  }
+  if (lane == 0) st_relaxed(&status[tile], lb_pack(epoch, 1, agg));
+  uint64_t prefix = 0;
+  int64_t base = (int64_t)tile - 1;
+  const uint32_t ep = epoch & 0xffffffu;
+  for (;;) {
+    const int64_t j = base - lane;
+    uint64_t w = 0;
+    uint32_t flag;
+    for (;;) {
+      if (j >= 0) {
+        w = ld_relaxed(&status[j]);
+        flag = ((uint32_t)(w >> 40) == ep) ? (uint32_t)((w >> 38) & 3u) : 0u;
+      } else {
+        w = 0;
+        flag = 2;
+      }
+      if (!__any_sync(0xffffffffu, flag == 0)) break;
+      __nanosleep(32);
+    }
+    const unsigned incl = __ballot_sync(0xffffffffu, flag == 2);
+    const int first = incl ? (__ffs(incl) - 1) : 32;
+    uint64_t v = (lane <= first) ? (w & ((1ull << 38) - 1)) : 0ull;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    prefix += v;
+    if (incl) break;
+    base -= 32;
+  }
+  if (lane == 0) st_relaxed(&status[tile], lb_pack(epoch, 2, prefix + agg));
+  return prefix;
+}
+
+}  // namespace dev
+}  // namespace isf

@@ -1,0 +1,713 @@
+// isf_lossy.cu -- host side of the C ABI (include/isf_lossy.h): plans, GLL
+// operators, launch configuration, error mapping, host-buffer entry points and
+// the NCCL reduction.  Kernels live in dlt_kernels.cuh.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/isf_lossy.h"
+#include "dlt_kernels.cuh"
+
+using namespace isf::dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = std::string(isf_lossy_error_code_name(code)) + ": " + buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(ISF_E_TASK_FAILED, "%s failed: %s", #expr, cudaGetErrorString(_e));     \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// GLL operators in long double (same recipe as DESIGN.md 3.1-3.2): nodes are
+// +-1 and the roots of P'_N by Newton, mirrored exactly; weights 2/(N(N+1)P_N^2);
+// F[k][i] = w_i L_k(x_i)/sqrt(g_k), B[i][k] = L_k(x_i)/sqrt(g_k), g_k = 2/(2k+1),
+// g_N = 2/N; parity (-1)^k enforced bitwise by mirroring.
+// ---------------------------------------------------------------------------
+void legendre_ld(int N, long double x, long double* P) {
+  P[0] = 1.0L;
+  if (N >= 1) P[1] = x;
+  for (int k = 2; k <= N; ++k)
+    P[k] = ((long double)(2 * k - 1) * x * P[k - 1] - (long double)(k - 1) * P[k - 2]) / (long double)k;
+}
+
+void gll_nodes_ld(int lx, long double* x, long double* w) {
+  const int N = lx - 1;
+  long double P[kMaxLx + 1];
+  for (int i = 0; i <= N; ++i) {
+    long double xi = -cosl(3.14159265358979323846264338327950288L * (long double)i / (long double)N);
+    for (int it = 0; it < 100; ++it) {
+      legendre_ld(N, xi, P);
+      const long double dx = (xi * P[N] - P[N - 1]) / ((long double)(N + 1) * P[N]);
+      xi -= dx;
+      if (fabsl(dx) < 1e-30L) break;
+    }
+    x[i] = xi;
+  }
+  x[0] = -1.0L;
+  x[N] = 1.0L;
+  for (int i = 0; i < lx / 2; ++i) x[N - i] = -x[i];
+  if (lx % 2) x[lx / 2] = 0.0L;
+  for (int i = 0; i <= N; ++i) {
+    legendre_ld(N, x[i], P);
+    w[i] = 2.0L / ((long double)N * (long double)(N + 1) * P[N] * P[N]);
+  }
+  for (int i = 0; i < lx / 2; ++i) w[N - i] = w[i];
+}
+
+void build_operators(int lx, double* F, double* B, double* xd, double* wd) {
+  const int N = lx - 1;
+  long double x[kMaxLx], w[kMaxLx], P[kMaxLx + 1];
+  gll_nodes_ld(lx, x, w);
+  for (int i = 0; i < lx; ++i) {
+    if (xd) xd[i] = (double)x[i];
+    if (wd) wd[i] = (double)w[i];
+  }
+  for (int i = 0; i < (lx + 1) / 2; ++i) {
+    legendre_ld(N, x[i], P);
+    for (int k = 0; k < lx; ++k) {
+      const long double g = (k < N) ? 2.0L / (long double)(2 * k + 1) : 2.0L / (long double)N;
+      const long double rs = 1.0L / sqrtl(g);
+      double f = (double)(w[i] * P[k] * rs);
+      double b = (double)(P[k] * rs);
+      if ((lx % 2) && i == lx / 2 && (k % 2)) { f = 0.0; b = 0.0; }
+      F[k * lx + i] = f;
+      B[i * lx + k] = b;
+      if (i != N - i) {
+        F[k * lx + (N - i)] = (k % 2) ? -f : f;
+        B[(N - i) * lx + k] = (k % 2) ? -b : b;
+      }
+    }
+  }
+}
+
+std::mutex g_init_mu;
+bool g_dev_init[64] = {};
+
+int init_device_constants(int device) {
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (device < 0 || device >= 64) return fail(ISF_E_INVALID_ARGUMENT, "device %d out of range", device);
+  if (g_dev_init[device]) return 0;
+  static double ops[kOpTableSize], ws[kWTableSize], xs[kWTableSize];
+  for (int lx = 2; lx <= kMaxLx; ++lx) {
+    double x[kMaxLx], w[kMaxLx];
+    build_operators(lx, ops + op_offset(lx), ops + op_offset(lx) + lx * lx, x, w);
+    for (int i = 0; i < lx; ++i) { ws[w_offset(lx) + i] = w[i]; xs[w_offset(lx) + i] = x[i]; }
+  }
+  CUDA_TRY(cudaMemcpyToSymbol(c_ops, ops, sizeof ops));
+  CUDA_TRY(cudaMemcpyToSymbol(c_w, ws, sizeof ws));
+  CUDA_TRY(cudaMemcpyToSymbol(c_x, xs, sizeof xs));
+  g_dev_init[device] = true;
+  return 0;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+uint64_t header_bytes(uint32_t P, uint64_t nblocks) {
+  const uint64_t W = ((uint64_t)P * P * P + 63) / 64;
+  return ((4 * nblocks + 7) & ~7ull) + 8 * W * nblocks;
+}
+
+}  // namespace
+
+struct isf_lossy_plan {
+  int device = 0;
+  uint32_t P = 0, comps = 0;
+  int sms = 0;
+  uint64_t* status = nullptr;
+  size_t status_cap = 0;
+  double* partials = nullptr;
+  size_t partials_cap = 0;  // slots of 4 doubles
+  uint32_t* counter = nullptr;
+  unsigned long long* flags = nullptr;
+  isf_lossy_stats* d_stats = nullptr;
+  isf_lossy_stats* h_stats = nullptr;  // pinned
+  uint32_t epoch = 0;
+  int last_launches = 0;
+  double F[kMaxLx * kMaxLx], B[kMaxLx * kMaxLx], x[kMaxLx], w[kMaxLx];
+  // host-path staging
+  void* d_in = nullptr;
+  size_t d_in_cap = 0;
+  void* d_out = nullptr;
+  size_t d_out_cap = 0;
+  void* d_aux = nullptr;
+  size_t d_aux_cap = 0;
+  cudaStream_t host_stream = nullptr;
+  int grid8c = 0, grid8d = 0, gridg = 0;
+  size_t smem_g = 0;
+};
+
+namespace {
+
+int ensure(isf_lossy_plan* p, size_t ntiles, size_t nparts) {
+  if (ntiles > p->status_cap) {
+    if (p->status) cudaFree(p->status);
+    size_t cap = std::max<size_t>(ntiles, 1024);
+    CUDA_TRY(cudaMalloc(&p->status, cap * sizeof(uint64_t)));
+    CUDA_TRY(cudaMemset(p->status, 0, cap * sizeof(uint64_t)));
+    p->status_cap = cap;
+  }
+  if (nparts > p->partials_cap) {
+    if (p->partials) cudaFree(p->partials);
+    size_t cap = std::max<size_t>(nparts, 1024);
+    CUDA_TRY(cudaMalloc(&p->partials, cap * 4 * sizeof(double)));
+    p->partials_cap = cap;
+  }
+  return 0;
+}
+
+uint32_t next_epoch(isf_lossy_plan* p, cudaStream_t s) {
+  p->epoch = (p->epoch + 1) & 0xffffffu;
+  if (p->epoch == 0) {  // wrapped: clear stale descriptors
+    cudaMemsetAsync(p->status, 0, p->status_cap * sizeof(uint64_t), s);
+    p->epoch = 1;
+  }
+  return p->epoch;
+}
+
+template <int LX>
+size_t gen_smem() { return GenSmem<LX>::bytes; }
+
+template <int LX>
+int launch_compress_generic(isf_lossy_plan* p, CompressArgs a, cudaStream_t s) {
+  const size_t sm = GenSmem<LX>::bytes;
+  static bool attr_set[64] = {};
+  if (!attr_set[p->device]) {
+    CUDA_TRY(cudaFuncSetAttribute(compress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CUDA_TRY(cudaFuncSetAttribute(decompress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr_set[p->device] = true;
+  }
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress_generic<LX>, kGenThreads, sm));
+  occ = std::max(occ, 1);
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->sms * occ, a.ws.ntiles ? a.ws.ntiles : 1);
+  a.ws.total_warps = grid;
+  compress_generic<LX><<<grid, kGenThreads, sm, s>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <int LX>
+int launch_decompress_generic(isf_lossy_plan* p, DecompressArgs a, cudaStream_t s, uint32_t* grid_out) {
+  const size_t sm = GenSmem<LX>::bytes;
+  static bool attr_set[64] = {};
+  if (!attr_set[p->device]) {
+    CUDA_TRY(cudaFuncSetAttribute(compress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CUDA_TRY(cudaFuncSetAttribute(decompress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr_set[p->device] = true;
+  }
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress_generic<LX>, kGenThreads, sm));
+  occ = std::max(occ, 1);
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->sms * occ, a.ws.ntiles ? a.ws.ntiles : 1);
+  a.ws.total_warps = grid;
+  *grid_out = grid;
+  decompress_generic<LX><<<grid, kGenThreads, sm, s>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+template <int... Ls>
+struct LxList {};
+
+template <int L0, int... Ls>
+int dispatch_compress_generic(LxList<L0, Ls...>, int lx, isf_lossy_plan* p, const CompressArgs& a, cudaStream_t s) {
+  if (lx == L0) return launch_compress_generic<L0>(p, a, s);
+  if constexpr (sizeof...(Ls) > 0) return dispatch_compress_generic(LxList<Ls...>{}, lx, p, a, s);
+  return fail(ISF_E_INVALID_ARGUMENT, "unsupported P=%d", lx);
+}
+template <int L0, int... Ls>
+int dispatch_decompress_generic(LxList<L0, Ls...>, int lx, isf_lossy_plan* p, const DecompressArgs& a,
+                                cudaStream_t s, uint32_t* g) {
+  if (lx == L0) return launch_decompress_generic<L0>(p, a, s, g);
+  if constexpr (sizeof...(Ls) > 0) return dispatch_decompress_generic(LxList<Ls...>{}, lx, p, a, s, g);
+  return fail(ISF_E_INVALID_ARGUMENT, "unsupported P=%d", lx);
+}
+using AllLx = LxList<2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>;
+
+bool use_fast8(const isf_lossy_plan* p) { return p->P == 8 && p->comps == 1; }
+
+int check_plan(const isf_lossy_plan* p) {
+  if (!p) return fail(ISF_E_INVALID_ARGUMENT, "null plan");
+  return 0;
+}
+
+uint64_t eps_q_of(double max_error) {
+  const double e2 = max_error * max_error;
+  return (uint64_t)ldexp(e2, 64);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* isf_lossy_last_error(void) { return g_last_error.c_str(); }
+
+const char* isf_lossy_error_code_name(int status) {
+  static const char* names[] = {"BadMagic", "UnsupportedVersion", "LengthMismatch", "ChecksumMismatch",
+                                "SerializationFailed", "ConnectFailed", "VersionMismatch", "InvalidCapacity",
+                                "ReaderGone", "WriterGone", "StagingError", "CalibrationFailed",
+                                "ShapeMismatch", "UnknownCodec", "DegenerateRange", "InvalidCadence",
+                                "DegenerateSamples", "TaskFailed", "ConsumerCrashed", "ConfigError",
+                                "InvalidArgument"};
+  if (status == 0) return "Ok";
+  if (status >= 1 && status <= 21) return names[status - 1];
+  return "UnknownError";
+}
+
+double isf_lossy_compression_ratio(uint64_t original_size, uint64_t compressed_size) {
+  return ((double)original_size - (double)compressed_size) / (double)original_size;
+}
+
+uint64_t isf_lossy_stream_header_bytes(uint32_t P, uint32_t comps, uint64_t n_elements) {
+  return header_bytes(P, n_elements * comps);
+}
+
+uint64_t isf_lossy_stream_capacity(uint32_t P, uint32_t comps, uint64_t n_elements) {
+  const uint64_t B = n_elements * comps;
+  return header_bytes(P, B) + 8ull * P * P * P * B;
+}
+
+int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int device) {
+  if (!out) return fail(ISF_E_INVALID_ARGUMENT, "null output pointer");
+  *out = nullptr;
+  if (P < 2 || P > (uint32_t)kMaxLx)
+    return fail(ISF_E_INVALID_ARGUMENT, "points_per_element_axis must be in [2,%d], got %u", kMaxLx, P);
+  if (comps != 1 && comps != 3) return fail(ISF_E_INVALID_ARGUMENT, "components must be 1 or 3, got %u", comps);
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(ISF_E_INVALID_ARGUMENT, "device %d not present (%d devices)", device, ndev);
+  DeviceGuard dg(device);
+  if (int rc = init_device_constants(device)) return rc;
+  auto* p = new isf_lossy_plan();
+  p->device = device;
+  p->P = P;
+  p->comps = comps;
+  CUDA_TRY(cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device));
+  CUDA_TRY(cudaMalloc(&p->counter, 64));
+  CUDA_TRY(cudaMemset(p->counter, 0, 64));
+  CUDA_TRY(cudaMalloc(&p->flags, 64));
+  CUDA_TRY(cudaMemset(p->flags, 0, 64));
+  CUDA_TRY(cudaMalloc(&p->d_stats, sizeof(isf_lossy_stats)));
+  CUDA_TRY(cudaMallocHost(&p->h_stats, sizeof(isf_lossy_stats)));
+  build_operators((int)P, p->F, p->B, p->x, p->w);
+  if (use_fast8(p)) {
+    CUDA_TRY(cudaFuncSetAttribute(compress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarps8 * kWarpBytes8));
+    CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarps8 * kWarpBytesD8));
+    int occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel, kWarps8 * 32, kWarps8 * kWarpBytes8));
+    p->grid8c = p->sms * std::max(occ, 1);
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel, kWarps8 * 32, kWarps8 * kWarpBytesD8));
+    p->grid8d = p->sms * std::max(occ, 1);
+  }
+  CUDA_TRY(ensure(p, 1 << 16, 1 << 14) == 0 ? cudaSuccess : cudaErrorMemoryAllocation);
+  *out = p;
+  return 0;
+}
+
+int isf_lossy_plan_destroy(isf_lossy_plan* p) {
+  if (!p) return 0;
+  DeviceGuard dg(p->device);
+  cudaFree(p->status);
+  cudaFree(p->partials);
+  cudaFree(p->counter);
+  cudaFree(p->flags);
+  cudaFree(p->d_stats);
+  cudaFreeHost(p->h_stats);
+  cudaFree(p->d_in);
+  cudaFree(p->d_out);
+  cudaFree(p->d_aux);
+  if (p->host_stream) cudaStreamDestroy(p->host_stream);
+  delete p;
+  return 0;
+}
+
+int isf_lossy_plan_operators(const isf_lossy_plan* p, double* F, double* B, double* x, double* w) {
+  if (int rc = check_plan(p)) return rc;
+  const int n = (int)p->P;
+  if (F) memcpy(F, p->F, sizeof(double) * n * n);
+  if (B) memcpy(B, p->B, sizeof(double) * n * n);
+  if (x) memcpy(x, p->x, sizeof(double) * n);
+  if (w) memcpy(w, p->w, sizeof(double) * n);
+  return 0;
+}
+
+int isf_lossy_plan_last_launches(const isf_lossy_plan* p) { return p ? p->last_launches : -1; }
+
+int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t n_elements, double max_error,
+                             int error_norm, void* d_stream, uint64_t capacity, isf_lossy_stats* d_stats,
+                             void* cuda_stream) {
+  if (int rc = check_plan(p)) return rc;
+  if (!(max_error > 0.0 && max_error < 1.0))
+    return fail(ISF_E_INVALID_ARGUMENT, "LossyConfig: max_error must be in (0,1), got %g", max_error);
+  if (error_norm != ISF_NORM_RELATIVE_L2)
+    return fail(ISF_E_INVALID_ARGUMENT, "LossyConfig: only RelativeL2 truncation is implemented (norm=%d)", error_norm);
+  if (n_elements == 0) return fail(ISF_E_INVALID_ARGUMENT, "empty field (0 elements)");
+  if (!d_field || !d_stream || !d_stats) return fail(ISF_E_INVALID_ARGUMENT, "null device pointer");
+  if (((uintptr_t)d_field & 15) || ((uintptr_t)d_stream & 15))
+    return fail(ISF_E_INVALID_ARGUMENT, "field and stream must be 16-byte aligned");
+  const uint64_t B = n_elements * p->comps;
+  const uint64_t hdr = header_bytes(p->P, B);
+  if (capacity < hdr) return fail(ISF_E_SERIALIZATION_FAILED, "capacity %llu < stream header %llu",
+                                  (unsigned long long)capacity, (unsigned long long)hdr);
+  DeviceGuard dg(p->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const bool fast = use_fast8(p);
+  const uint64_t ntiles64 = fast ? (B + 3) / 4 : B;
+  if (ntiles64 >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
+  const uint32_t ntiles = (uint32_t)ntiles64;
+  if (int rc = ensure(p, ntiles, ntiles)) return rc;
+  CompressArgs a;
+  a.field = d_field;
+  a.nblocks = B;
+  a.comps = (int)p->comps;
+  a.stream = (uint8_t*)d_stream;
+  a.cap = capacity;
+  a.mask_off = (4 * B + 7) & ~7ull;
+  a.val_off = hdr;
+  a.eps_q = eps_q_of(max_error);
+  a.ws = Workspace{p->status, p->partials, p->counter, p->flags, next_epoch(p, s), ntiles, 0};
+  if (fast) {
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8c, (ntiles + kWarps8 - 1) / kWarps8);
+    a.ws.total_warps = grid * kWarps8;
+    compress8_kernel<<<grid, kWarps8 * 32, kWarps8 * kWarpBytes8, s>>>(a);
+    CUDA_TRY(cudaGetLastError());
+  } else {
+    if (int rc = dispatch_compress_generic(AllLx{}, (int)p->P, p, a, s)) return rc;
+  }
+  FinalizeArgs f{0, p->partials, ntiles, p->status, ntiles, p->flags, d_stats, B,
+                 B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
+  finalize_kernel<<<1, kFinThreads, 0, s>>>(f);
+  CUDA_TRY(cudaGetLastError());
+  p->last_launches = 2;
+  return 0;
+}
+
+static int status_to_rc_compress(const isf_lossy_stats& st) {
+  if (st.status & ISF_STATUS_NONFINITE) return fail(ISF_E_INVALID_ARGUMENT, "Field: non-finite value");
+  if (st.status & ISF_STATUS_OVERFLOW)
+    return fail(ISF_E_SERIALIZATION_FAILED, "stream capacity too small (need %llu bytes)",
+                (unsigned long long)st.stream_bytes);
+  return 0;
+}
+
+int isf_lossy_compress(isf_lossy_plan* p, const double* d_field, uint64_t n_elements, double max_error,
+                       int error_norm, void* d_stream, uint64_t capacity, uint64_t* stream_bytes,
+                       isf_lossy_stats* stats, void* cuda_stream) {
+  if (int rc = check_plan(p)) return rc;
+  DeviceGuard dg(p->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (int rc = isf_lossy_compress_async(p, d_field, n_elements, max_error, error_norm, d_stream, capacity,
+                                        p->d_stats, cuda_stream))
+    return rc;
+  CUDA_TRY(cudaMemcpyAsync(p->h_stats, p->d_stats, sizeof(isf_lossy_stats), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (stats) *stats = *p->h_stats;
+  if (stream_bytes) *stream_bytes = p->h_stats->stream_bytes;
+  return status_to_rc_compress(*p->h_stats);
+}
+
+int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t stream_bytes, uint64_t n_elements,
+                               double* d_out, const double* d_original, isf_lossy_stats* d_stats,
+                               void* cuda_stream) {
+  if (int rc = check_plan(p)) return rc;
+  if (n_elements == 0) return fail(ISF_E_INVALID_ARGUMENT, "empty field (0 elements)");
+  if (!d_stream || !d_out || !d_stats) return fail(ISF_E_INVALID_ARGUMENT, "null device pointer");
+  if (((uintptr_t)d_out & 15) || ((uintptr_t)d_stream & 15) || ((uintptr_t)d_original & 15))
+    return fail(ISF_E_INVALID_ARGUMENT, "stream, output and original must be 16-byte aligned");
+  const uint64_t B = n_elements * p->comps;
+  const uint64_t hdr = header_bytes(p->P, B);
+  if (stream_bytes < hdr)
+    return fail(ISF_E_SHAPE_MISMATCH, "stream of %llu bytes is shorter than its header (%llu bytes) for %llu elements",
+                (unsigned long long)stream_bytes, (unsigned long long)hdr, (unsigned long long)n_elements);
+  DeviceGuard dg(p->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const bool fast = use_fast8(p);
+  const uint64_t ntiles64 = fast ? (B + 3) / 4 : B;
+  if (ntiles64 >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
+  const uint32_t ntiles = (uint32_t)ntiles64;
+  const size_t nparts = fast ? (size_t)p->grid8d * kWarps8 : (size_t)p->sms * 16;
+  if (int rc = ensure(p, ntiles, nparts)) return rc;
+  DecompressArgs a;
+  a.stream = (const uint8_t*)d_stream;
+  a.stream_bytes = stream_bytes;
+  a.nblocks = B;
+  a.comps = (int)p->comps;
+  a.mask_off = (4 * B + 7) & ~7ull;
+  a.val_off = hdr;
+  a.out = d_out;
+  a.orig = d_original;
+  a.ws = Workspace{p->status, p->partials, p->counter, p->flags, next_epoch(p, s), ntiles, 0};
+  uint32_t grid = 0, parts = 0;
+  if (fast) {
+    grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8d, (ntiles + kWarps8 - 1) / kWarps8);
+    a.ws.total_warps = grid * kWarps8;
+    decompress8_kernel<<<grid, kWarps8 * 32, kWarps8 * kWarpBytesD8, s>>>(a);
+    CUDA_TRY(cudaGetLastError());
+    parts = grid * kWarps8;
+  } else {
+    if (int rc = dispatch_decompress_generic(AllLx{}, (int)p->P, p, a, s, &grid)) return rc;
+    parts = grid;
+  }
+  FinalizeArgs f{1, p->partials, d_original ? parts : 0u, p->status, ntiles, p->flags, d_stats, B,
+                 B * (uint64_t)p->P * p->P * p->P * 8, hdr, d_original ? 1 : 0};
+  finalize_kernel<<<1, kFinThreads, 0, s>>>(f);
+  CUDA_TRY(cudaGetLastError());
+  p->last_launches = 2;
+  return 0;
+}
+
+int isf_lossy_decompress(isf_lossy_plan* p, const void* d_stream, uint64_t stream_bytes, uint64_t n_elements,
+                         double* d_out, const double* d_original, isf_lossy_stats* stats, void* cuda_stream) {
+  if (int rc = check_plan(p)) return rc;
+  DeviceGuard dg(p->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (int rc = isf_lossy_decompress_async(p, d_stream, stream_bytes, n_elements, d_out, d_original, p->d_stats,
+                                          cuda_stream))
+    return rc;
+  CUDA_TRY(cudaMemcpyAsync(p->h_stats, p->d_stats, sizeof(isf_lossy_stats), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  isf_lossy_stats st = *p->h_stats;
+  if (stats) *stats = st;
+  if ((st.status & ISF_STATUS_SHAPE) || st.stream_bytes != stream_bytes)
+    return fail(ISF_E_SHAPE_MISMATCH, "stream inconsistent with shape (%llu elements of P=%u): %llu bytes given, %llu implied",
+                (unsigned long long)n_elements, p->P, (unsigned long long)stream_bytes,
+                (unsigned long long)st.stream_bytes);
+  return 0;
+}
+
+static int grow(void** ptr, size_t* cap, size_t need) {
+  if (need <= *cap) return 0;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *cap = 0;
+  CUDA_TRY(cudaMalloc(ptr, need));
+  *cap = need;
+  return 0;
+}
+
+int isf_lossy_compress_host(isf_lossy_plan* p, const double* h_field, uint64_t n_elements, double max_error,
+                            int error_norm, void* h_stream, uint64_t capacity, uint64_t* stream_bytes,
+                            isf_lossy_stats* stats) {
+  if (int rc = check_plan(p)) return rc;
+  if (!h_field || !h_stream) return fail(ISF_E_INVALID_ARGUMENT, "null host pointer");
+  DeviceGuard dg(p->device);
+  if (!p->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->host_stream, cudaStreamNonBlocking));
+  const uint64_t fbytes = n_elements * p->comps * (uint64_t)p->P * p->P * p->P * 8;
+  const uint64_t cap = std::min<uint64_t>(capacity, isf_lossy_stream_capacity(p->P, p->comps, n_elements));
+  if (int rc = grow(&p->d_in, &p->d_in_cap, fbytes)) return rc;
+  if (int rc = grow(&p->d_out, &p->d_out_cap, cap)) return rc;
+  cudaStream_t s = p->host_stream;
+  CUDA_TRY(cudaMemcpyAsync(p->d_in, h_field, fbytes, cudaMemcpyHostToDevice, s));
+  uint64_t nb = 0;
+  isf_lossy_stats st;
+  int rc = isf_lossy_compress(p, (const double*)p->d_in, n_elements, max_error, error_norm, p->d_out, cap, &nb,
+                              &st, s);
+  if (stats) *stats = st;
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(h_stream, p->d_out, nb, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (stream_bytes) *stream_bytes = nb;
+  return 0;
+}
+
+int isf_lossy_decompress_host(isf_lossy_plan* p, const void* h_stream, uint64_t stream_bytes, uint64_t n_elements,
+                              double* h_out, const double* h_original, isf_lossy_stats* stats) {
+  if (int rc = check_plan(p)) return rc;
+  if (!h_stream || !h_out) return fail(ISF_E_INVALID_ARGUMENT, "null host pointer");
+  DeviceGuard dg(p->device);
+  if (!p->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->host_stream, cudaStreamNonBlocking));
+  const uint64_t fbytes = n_elements * p->comps * (uint64_t)p->P * p->P * p->P * 8;
+  const size_t sb = (stream_bytes + 15) & ~15ull;
+  if (int rc = grow(&p->d_in, &p->d_in_cap, sb)) return rc;
+  if (int rc = grow(&p->d_out, &p->d_out_cap, fbytes)) return rc;
+  if (h_original) {
+    if (int rc = grow(&p->d_aux, &p->d_aux_cap, fbytes)) return rc;
+  }
+  cudaStream_t s = p->host_stream;
+  CUDA_TRY(cudaMemcpyAsync(p->d_in, h_stream, stream_bytes, cudaMemcpyHostToDevice, s));
+  if (h_original) CUDA_TRY(cudaMemcpyAsync(p->d_aux, h_original, fbytes, cudaMemcpyHostToDevice, s));
+  isf_lossy_stats st;
+  int rc = isf_lossy_decompress(p, p->d_in, stream_bytes, n_elements, (double*)p->d_out,
+                                h_original ? (const double*)p->d_aux : nullptr, &st, s);
+  if (stats) *stats = st;
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(h_out, p->d_out, fbytes, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return 0;
+}
+
+// ---- NCCL (resolved at run time) ----
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_group_fn)(void);
+
+int isf_lossy_allreduce(isf_lossy_stats* d_stats, void* comm, void* cuda_stream) {
+  if (!d_stats || !comm) return fail(ISF_E_INVALID_ARGUMENT, "null stats or communicator");
+  static nccl_allreduce_fn ar = nullptr;
+  static nccl_group_fn gs = nullptr, ge = nullptr;
+  if (!ar) {
+    ar = (nccl_allreduce_fn)dlsym(RTLD_DEFAULT, "ncclAllReduce");
+    gs = (nccl_group_fn)dlsym(RTLD_DEFAULT, "ncclGroupStart");
+    ge = (nccl_group_fn)dlsym(RTLD_DEFAULT, "ncclGroupEnd");
+    if (!ar) {
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (h) {
+        ar = (nccl_allreduce_fn)dlsym(h, "ncclAllReduce");
+        gs = (nccl_group_fn)dlsym(h, "ncclGroupStart");
+        ge = (nccl_group_fn)dlsym(h, "ncclGroupEnd");
+      }
+    }
+    if (!ar || !gs || !ge) return fail(ISF_E_TASK_FAILED, "NCCL not found in the process");
+  }
+  // ncclDataType_t: ncclUint64 = 5, ncclFloat64 = 8; ncclRedOp_t: ncclSum = 0, ncclMax = 2
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  double* d = reinterpret_cast<double*>(d_stats);
+  uint64_t* u = reinterpret_cast<uint64_t*>(d_stats);
+  int r = gs();
+  r |= ar(d + 0, d + 0, 2, 8, 0, comm, s);   // err2, nrm2
+  r |= ar(d + 2, d + 2, 2, 8, 2, comm, s);   // err_inf, u_inf
+  r |= ar(d + 4, d + 4, 2, 8, 0, comm, s);   // disc2, tot2
+  r |= ar(u + 6, u + 6, 4, 5, 0, comm, s);   // kept, blocks, stream_bytes, field_bytes
+  r |= ar(u + 10, u + 10, 1, 5, 2, comm, s); // status (bit flags: max of small ints ~ or)
+  r |= ge();
+  if (r) return fail(ISF_E_TASK_FAILED, "ncclAllReduce failed (%d)", r);
+  return 0;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Synthetic in-situ producers.  Not on the timed path.
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ double Wg_node(int P, int i) { return c_x[w_offset(P) + i]; }
+
+__global__ void tgv_kernel(double* out, uint32_t E, uint32_t ez0, uint64_t nel, int P, int which, double h) {
+  const uint64_t n3 = (uint64_t)P * P * P;
+  const uint64_t total = nel * n3;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = t / n3, p = t % n3;
+    const uint64_t ex = e % E, ey = (e / E) % E, ez = e / ((uint64_t)E * E) + ez0;
+    const int px = (int)(p % P), py = (int)((p / P) % P), pz = (int)(p / ((uint64_t)P * P));
+    const double rx = (Wg_node(P, px) + 1.0) * 0.5 * h, ry = (Wg_node(P, py) + 1.0) * 0.5 * h,
+                 rz = (Wg_node(P, pz) + 1.0) * 0.5 * h;
+    const double x = (double)ex * h + rx, y = (double)ey * h + ry, z = (double)ez * h + rz;
+    double v;
+    switch (which) {
+      case 0: v = cos(x) * sin(y) * sin(z); break;
+      case 1: v = -sin(x) * cos(y) * sin(z); break;
+      case 2: v = 0.0; break;
+      default: v = (cos(2.0 * x) + cos(2.0 * y)) * (cos(2.0 * z) + 2.0) / 16.0; break;
+    }
+    out[t] = v;
+  }
+}
+
+__device__ __forceinline__ void philox(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+    const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+// dense stream: counts = n3, masks all ones, values = (2U-1)*amp[j]
+__global__ void spectral_stream_kernel(uint8_t* stream, uint64_t nblocks, uint64_t block0, int n3, int W,
+                                       uint64_t mask_off, uint64_t val_off, uint64_t seed, const double* amp) {
+  uint32_t* counts = reinterpret_cast<uint32_t*>(stream);
+  uint64_t* masks = reinterpret_cast<uint64_t*>(stream + mask_off);
+  double* vals = reinterpret_cast<double*>(stream + val_off);
+  const uint64_t lastmask = (n3 % 64) ? ((1ull << (n3 % 64)) - 1ull) : ~0ull;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nblocks * n3; t += stride) {
+    const uint64_t b = t / n3;
+    const uint32_t j = (uint32_t)(t % n3);
+    const uint64_t gblk = block0 + b;
+    uint32_t c[4] = {(uint32_t)gblk, (uint32_t)(gblk >> 32), j, 0u};
+    philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint64_t M = ((uint64_t)c[0] << 21) | (c[1] >> 11);
+    const double U2 = ldexp((double)(int64_t)(2 * M) - 9007199254740992.0, -53);
+    vals[t] = __dmul_rn(U2, amp[j]);
+    if (j == 0) {
+      counts[b] = (uint32_t)n3;
+      if (b + 1 == nblocks && (nblocks & 1)) counts[b + 1] = 0;
+    }
+    if (j < (uint32_t)W) masks[b * W + j] = (j == (uint32_t)W - 1) ? lastmask : ~0ull;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int isf_lossy_generate_tgv(isf_lossy_plan* p, double* d_out, uint32_t E_ax, uint32_t ez0, uint32_t nz, int which,
+                           double domain, void* cuda_stream) {
+  if (int rc = check_plan(p)) return rc;
+  if (p->comps != 1) return fail(ISF_E_INVALID_ARGUMENT, "TGV generator writes scalar fields (components=1)");
+  DeviceGuard dg(p->device);
+  const uint64_t nel = (uint64_t)E_ax * E_ax * nz;
+  tgv_kernel<<<p->sms * 8, 256, 0, (cudaStream_t)cuda_stream>>>(d_out, E_ax, ez0, nel, (int)p->P, which,
+                                                                  domain / (double)E_ax);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int isf_lossy_generate_spectral(isf_lossy_plan* p, double* d_out, uint64_t block0, uint64_t nblocks, uint64_t seed,
+                                const double* h_amp, void* cuda_stream) {
+  if (int rc = check_plan(p)) return rc;
+  if (p->comps != 1) return fail(ISF_E_INVALID_ARGUMENT, "spectral generator writes scalar fields (components=1)");
+  DeviceGuard dg(p->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const int n3 = (int)(p->P * p->P * p->P), W = (n3 + 63) / 64;
+  const uint64_t bytes = isf_lossy_stream_capacity(p->P, 1, nblocks);
+  void* tmp = nullptr;
+  double* d_amp = nullptr;
+  CUDA_TRY(cudaMallocAsync(&tmp, bytes, s));
+  CUDA_TRY(cudaMallocAsync((void**)&d_amp, sizeof(double) * n3, s));
+  CUDA_TRY(cudaMemcpyAsync(d_amp, h_amp, sizeof(double) * n3, cudaMemcpyHostToDevice, s));
+  spectral_stream_kernel<<<p->sms * 8, 256, 0, s>>>((uint8_t*)tmp, nblocks, block0, n3, W, (4 * nblocks + 7) & ~7ull,
+                                                     header_bytes(p->P, nblocks), seed, d_amp);
+  CUDA_TRY(cudaGetLastError());
+  int rc = isf_lossy_decompress(p, tmp, bytes, nblocks, d_out, nullptr, nullptr, cuda_stream);
+  cudaFreeAsync(tmp, s);
+  cudaFreeAsync(d_amp, s);
+  return rc;
+}
+
+}  // extern "C"
