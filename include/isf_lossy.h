@@ -30,7 +30,7 @@
  *     (single-owner, like StageWriter).
  *
  * Stream format (little-endian, proj/include/isf/core/bytes.hpp:17-32):
- *   counts u32[B] | zero pad to 8 B | masks u64[B][W] | values f64[sum counts]
+ *   counts u32[B] | zero pad to 16 B | masks u64[B][W] | values f64[sum counts]
  *   B = elements * components blocks, block b = element*components + component,
  *   W = ceil(P^3/64), mask bit j (LSB first) <-> Legendre coefficient j =
  *   kx + P*(ky + P*kz); values in ascending j, blocks in order.

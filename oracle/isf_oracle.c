@@ -190,7 +190,7 @@ void iso_inv_block(int lx, const double* B, const double* a, double* u) {
 /*   s      = frexp exponent of max|a|   (2^(s-1) <= max|a| < 2^s)            */
 /*   a''_j  = |a_j| * 2^(K-s)            (exact whenever the result is >= 1)  */
 /*   e_j    = fl(a''_j * a''_j)  in [0, 2^50)                                 */
-/*   lo_j   = floor(e_j), hi_j = ceil(e_j)           (integers, u64)          */
+/*   lo_j   = floor(e_j), hi_j = lo_j + (a_j != 0)   (integers, u64)          */
 /*   T      = sum lo_j,  q = floor(fl(eps*eps) * 2^64),  thr = floor(T*q/2^64) */
 /*   discard order: |a| ascending, ties by index descending (= sort by |c|    */
 /*   descending, index ascending, read from the end)                         */
@@ -265,9 +265,8 @@ static uint32_t select_impl(int lx, const double* a, double max_error, double re
     for (int j = 0; j < n3; ++j) {
         double as = ldexp(fabs(a[j]), k);
         double e = as * as;
-        double fl = floor(e), ce = ceil(e);
-        lo[j] = (uint64_t)fl;
-        hi[j] = (uint64_t)ce;
+        lo[j] = (uint64_t)floor(e);
+        hi[j] = lo[j] + (a[j] != 0.0); /* upper bound of e; exact zeros cost nothing */
         T += lo[j];
         uint64_t b;
         memcpy(&b, &a[j], 8);
@@ -308,12 +307,12 @@ uint32_t iso_select_block_perturbed(int lx, const double* a, double max_error, d
 
 /* ------------------------------------------------------------------------- */
 /* Stream format, little-endian:                              */
-/*   counts u32[B] | pad to 8 | masks u64[B][W] | values f64[sum counts]      */
+/*   counts u32[B] | pad to 16 | masks u64[B][W] | values f64[sum counts]      */
 /* Block b = element*comps + comp; values in ascending coefficient index.     */
 /* ------------------------------------------------------------------------- */
 uint64_t iso_stream_header_bytes(int lx, uint64_t nblocks) {
     const uint64_t W = ((uint64_t)lx * lx * lx + 63) / 64;
-    return ((4 * nblocks + 7) & ~7ull) + 8 * W * nblocks;
+    return ((4 * nblocks + 15) & ~15ull) + 8 * W * nblocks;
 }
 
 uint64_t iso_stream_capacity(int lx, uint64_t nblocks) {
@@ -345,8 +344,8 @@ int iso_compress(int lx, int comps, uint64_t n_elements, const double* field, do
     double F[ISO_MAX_LX * ISO_MAX_LX], Bm[ISO_MAX_LX * ISO_MAX_LX];
     iso_matrices(lx, F, Bm);
     uint32_t* counts = (uint32_t*)stream;
-    uint64_t* masks = (uint64_t*)(stream + ((4 * B + 7) & ~7ull));
-    if (B & 1) counts[B] = 0; /* pad */
+    uint64_t* masks = (uint64_t*)(stream + ((4 * B + 15) & ~15ull));
+    for (uint64_t pb = B; pb < ((B + 3) & ~3ull); ++pb) counts[pb] = 0; /* pad to 16 B */
     const int nt = omp_threads(nthreads);
     double** tbuf = (double**)calloc((size_t)nt, sizeof(double*));
     uint64_t* tcount = (uint64_t*)calloc((size_t)nt, sizeof(uint64_t));
@@ -432,7 +431,7 @@ int iso_decompress(int lx, int comps, uint64_t n_elements, const uint8_t* stream
     const uint64_t hdr = iso_stream_header_bytes(lx, B);
     if (stream_bytes < hdr) return ERR_SHAPE;
     const uint32_t* counts = (const uint32_t*)stream;
-    const uint64_t* masks = (const uint64_t*)(stream + ((4 * B + 7) & ~7ull));
+    const uint64_t* masks = (const uint64_t*)(stream + ((4 * B + 15) & ~15ull));
     const double* vals = (const double*)(stream + hdr);
     const uint64_t lastmask = (n3 % 64) ? ((1ull << (n3 % 64)) - 1) : ~0ull;
     uint64_t* offs = (uint64_t*)malloc((B + 1) * sizeof(uint64_t));

@@ -205,7 +205,7 @@ def philox(ctr, key):
 def parse_stream(stream: np.ndarray, lx: int, nblocks: int):
     W = (lx ** 3 + 63) // 64
     c_end = 4 * nblocks
-    m0 = (c_end + 7) & ~7
+    m0 = (c_end + 15) & ~15
     counts = stream[:c_end].view(np.uint32)
     masks = stream[m0:m0 + 8 * W * nblocks].view(np.uint64).reshape(nblocks, W)
     vals = stream[m0 + 8 * W * nblocks:].view(np.float64)

@@ -111,7 +111,7 @@ __device__ __forceinline__ void inv_line_ptr(double* p, int stride) {
 
 // ---------------------------------------------------------------------------
 // Energy quantisation: e = fl((|a|*2^k)^2) < 2^50,
-// lo = floor(e), hi = ceil(e) via a directed-rounding add of 2^52.
+// lo = floor(e) via a round-down add of 2^52, hi = lo + (a != 0).
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int ceil_log2(int v) {
   int r = 0;
@@ -131,12 +131,12 @@ __device__ __forceinline__ uint64_t e_lo(double a, double f) {
   const double t = __dmul_rn(a, f);
   return low52(__dadd_rd(__dmul_rn(t, t), 4503599627370496.0));
 }
-__device__ __forceinline__ uint64_t e_hi(double a, double f) {
-  const double t = __dmul_rn(a, f);
-  return low52(__dadd_ru(__dmul_rn(t, t), 4503599627370496.0));
-}
 __device__ __forceinline__ uint64_t abs_bits(double a) {
   return (uint64_t)__double_as_longlong(a) & 0x7FFFFFFFFFFFFFFFull;
+}
+// upper bound of e used for discarded energy: floor(e) + 1, and 0 for an exact zero
+__device__ __forceinline__ uint64_t e_hi(double a, double f) {
+  return e_lo(a, f) + (abs_bits(a) != 0 ? 1ull : 0ull);
 }
 
 // ---------------------------------------------------------------------------
@@ -218,21 +218,21 @@ struct LaneGroup {
 };
 
 // ---------------------------------------------------------------------------
-// Exact selection, hard path: the candidates (keys = |a| bits, coefficient
-// indices) sit in shared memory; an MSB radix select with 64 energy-sum bins
-// finds the boundary key t* and the index cut of a tie group so that
+// Exact selection, general path: MSB radix select with 64 energy-sum bins.
+// Finds the boundary key t* and the index cut of a tie group so that
 //   kept  <=>  key > t*  ||  (key == t* && idx < icut)
 // and the discarded set is the longest prefix of the discard order (|a| asc,
-// index desc) with sum(hi) <= R.  Group = lanes of one warp (G <= 32).
+// index desc) with sum(hi) <= R.  `src(p, key, idx)` yields element p < n.
+// Group = G lanes of one warp.  hist: 64 u64 in shared memory.
 // ---------------------------------------------------------------------------
-template <int G>
-__device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const uint64_t* keys,
-                                          const uint16_t* idxs, int n, uint64_t R, double f,
-                                          unsigned long long* hist, uint64_t& tstar,
-                                          uint32_t& icut, uint64_t& dsum) {
+template <int G, class Src>
+__device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const Src& src, int n, uint64_t R,
+                                             double f, unsigned long long* hist, uint64_t& tstar,
+                                             uint32_t& icut, uint64_t& dsum) {
   uint64_t klo = ~0ull, khi = 0;
   for (int p = g.rank; p < n; p += G) {
-    const uint64_t k = keys[p];
+    uint64_t k; uint32_t ix;
+    src(p, k, ix);
     klo = k < klo ? k : klo;
     khi = k > khi ? k : khi;
   }
@@ -242,10 +242,10 @@ __device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const uint64
   for (;;) {
     const uint64_t span = khi - klo;
     if (span == 0) {
-      // tie group: every undecided candidate has key == klo
+      // tie group: every undecided element has key == klo
       const uint64_t h = e_hi(__longlong_as_double((long long)klo), f);
       uint32_t cnt = 0;
-      for (int p = g.rank; p < n; p += G) cnt += (keys[p] == klo);
+      for (int p = g.rank; p < n; p += G) { uint64_t k; uint32_t ix; src(p, k, ix); cnt += (k == klo); }
       const uint32_t gcount = g.sum(cnt);
       uint64_t r = (h == 0) ? gcount : (R / h);
       if (r > gcount) r = gcount;
@@ -260,10 +260,11 @@ __device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const uint64
         const uint32_t want = gcount - (uint32_t)r;
         uint32_t mine = 0xffffffffu;
         for (int p = g.rank; p < n; p += G) {
-          if (keys[p] != klo) continue;
-          const uint32_t ip = idxs[p];
+          uint64_t k; uint32_t ip;
+          src(p, k, ip);
+          if (k != klo) continue;
           uint32_t rank = 0;
-          for (int q = 0; q < n; ++q) rank += (keys[q] == klo && idxs[q] < ip);
+          for (int q = 0; q < n; ++q) { uint64_t kq; uint32_t iq; src(q, kq, iq); rank += (kq == klo && iq < ip); }
           if (rank == want) mine = ip;
         }
         icut = g.min(mine);
@@ -275,12 +276,12 @@ __device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const uint64
     for (int b = g.rank; b < 64; b += G) hist[b] = 0ull;
     g.sync();
     for (int p = g.rank; p < n; p += G) {
-      const uint64_t k = keys[p];
+      uint64_t k; uint32_t ix;
+      src(p, k, ix);
       if (k >= klo && k <= khi)
         atomicAdd(&hist[(k - klo) >> shift], (unsigned long long)e_hi(__longlong_as_double((long long)k), f));
     }
     g.sync();
-    // each lane owns 64/G consecutive bins
     constexpr int BPL = 64 / G;
     uint64_t loc[BPL];
     uint64_t run = 0;
@@ -310,12 +311,63 @@ __device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const uint64
     const uint64_t nhi = nhi_full < khi ? nhi_full : khi;
     uint64_t mn = ~0ull, mx = 0;
     for (int p = g.rank; p < n; p += G) {
-      const uint64_t k = keys[p];
+      uint64_t k; uint32_t ix;
+      src(p, k, ix);
       if (k >= nlo && k <= nhi) { mn = k < mn ? k : mn; mx = k > mx ? k : mx; }
     }
     klo = g.min(mn);
     khi = g.max(mx);
   }
+}
+
+// element sources for radix_select
+struct SrcCompacted {  // candidate keys + indices (generic kernels)
+  const uint64_t* keys;
+  const uint16_t* idxs;
+  __device__ __forceinline__ void operator()(int p, uint64_t& k, uint32_t& ix) const { k = keys[p]; ix = idxs[p]; }
+};
+struct SrcDense {  // raw coefficients in natural order, index = position (fast kernels)
+  const double* a;
+  __device__ __forceinline__ void operator()(int p, uint64_t& k, uint32_t& ix) const { k = abs_bits(a[p]); ix = (uint32_t)p; }
+};
+
+// ---------------------------------------------------------------------------
+// mbarrier + bulk async copy (TMA engine, cp.async.bulk) helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,612 @@
+// dlt_fast8.cuh -- lx = 8, scalar-field fast path (the north_star configuration).
+//
+// One warp processes one (element, component) block of 8^3 fp64 values at a time;
+// warps take blocks round-robin (block = gw, gw + W, ...), so there is no
+// inter-warp dependency inside the hot kernels.  Per warp a ring of 4 KiB
+// shared-memory stages is filled by the TMA engine (cp.async.bulk issued by one
+// lane, mbarrier completion) kF8Stages blocks ahead.
+//
+// Register layouts (lane l, 16 values per lane):
+//   z-lines : lane = (y = l>>2, q = l&3) holds x = 2q, 2q+1 at row y for all z
+//   y-lines : lane = (kz = l>>2, q = l&3) holds x = 2q, 2q+1 for all y at plane kz
+//   x-lines : lane = (kz = l>>2, p = l&3) holds ky = 2p, 2p+1 for all x at plane kz
+// so after the forward x sweep lane l owns coefficients 16 l .. 16 l + 15.
+// The two role changes are in-place shared-memory transpositions with the XOR
+// swizzle swz() on 16-byte chunks, bank-conflict free for all four access patterns.
+// Forward sweeps z, y, x; inverse x, y, z (the pinned order of oracle/isf_oracle.c).
+#pragma once
+#include "dlt_kernels.cuh"
+
+namespace isf {
+namespace dev {
+
+constexpr int kF8Warps = 16;   // warps per CTA
+constexpr int kF8Stages = 2;   // TMA ring depth per warp
+
+// 16-byte chunk c (0..31) of plane kz (512 B)
+__device__ __forceinline__ int swz(int kz, int c) { return c ^ (((c >> 3) & 3) | ((kz & 1) << 2)); }
+
+// warp sum of per-lane values < 2^58 via three 32-bit REDUX.SUM (exact)
+__device__ __forceinline__ uint64_t warp_sum_u58(uint64_t x) {
+  const uint32_t a = (uint32_t)(x & 0x3FFFFFFull);
+  const uint32_t b = (uint32_t)((x >> 26) & 0x3FFFFFFull);
+  const uint32_t c = (uint32_t)(x >> 52);
+  const uint64_t sa = __reduce_add_sync(0xffffffffu, a);
+  const uint64_t sb = __reduce_add_sync(0xffffffffu, b);
+  const uint64_t sc = __reduce_add_sync(0xffffffffu, c);
+  return sa + (sb << 26) + (sc << 52);
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t x) {
+  const uint32_t hi = (uint32_t)(x >> 32);
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t lo = hi == mh ? (uint32_t)x : 0u;
+  return ((uint64_t)mh << 32) | __reduce_max_sync(0xffffffffu, lo);
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t x) {
+  const uint32_t hi = (uint32_t)(x >> 32);
+  const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+  const uint32_t lo = hi == mh ? (uint32_t)x : 0xffffffffu;
+  return ((uint64_t)mh << 32) | __reduce_min_sync(0xffffffffu, lo);
+}
+__device__ __forceinline__ uint32_t warp_exscan_u32(uint32_t v, int lane) {
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  return x - v;
+}
+
+// ---------------------------------------------------------------------------
+// General-path exact selection over the warp's 512 coefficients held 16 per lane
+// (same algorithm as radix_select in dlt_common.cuh, elements in registers).
+// out = {t*, icut, discarded hi-sum}.
+// ---------------------------------------------------------------------------
+__device__ __noinline__ void radix_select16(const double* vin, int lane, uint64_t R, double f,
+                                            unsigned long long* hist, uint64_t* out) {
+  double v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = vin[r];
+  uint64_t klo = ~0ull, khi = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const uint64_t k = abs_bits(v[r]);
+    klo = k < klo ? k : klo;
+    khi = k > khi ? k : khi;
+  }
+  klo = warp_min_u64(klo);
+  khi = warp_max_u64(khi);
+  uint64_t dsum = 0;
+  for (;;) {
+    const uint64_t span = khi - klo;
+    if (span == 0) {
+      const uint64_t h = klo ? e_lo(__longlong_as_double((long long)klo), f) + 1 : 0ull;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) cnt += (abs_bits(v[r]) == klo);
+      const uint32_t gcount = __reduce_add_sync(0xffffffffu, cnt);
+      uint64_t rr = (h == 0) ? gcount : (R / h);
+      if (rr > gcount) rr = gcount;
+      dsum += rr * h;
+      uint32_t icut;
+      if (rr == gcount) {
+        icut = 0;
+      } else if (rr == 0) {
+        icut = 0xffffffffu;
+      } else {
+        // keep the (gcount - rr) smallest indices; tied elements are in ascending
+        // (lane, register) = index order
+        const uint32_t want = gcount - (uint32_t)rr;
+        const uint32_t below = warp_exscan_u32(cnt, lane);
+        uint32_t mine = 0xffffffffu, seen = 0;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if (abs_bits(v[r]) == klo) {
+            if (below + seen == want) mine = (uint32_t)(16 * lane + r);
+            ++seen;
+          }
+        icut = __reduce_min_sync(0xffffffffu, mine);
+      }
+      out[0] = klo;
+      out[1] = icut;
+      out[2] = dsum;
+      return;
+    }
+    const int bits = 64 - __clzll((long long)span);
+    const int shift = bits > 6 ? bits - 6 : 0;
+    hist[lane] = 0ull;
+    hist[lane + 32] = 0ull;
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint64_t k = abs_bits(v[r]);
+      if (k >= klo && k <= khi)
+        atomicAdd(&hist[(k - klo) >> shift], (unsigned long long)(e_lo(v[r], f) + 1ull));
+    }
+    __syncwarp();
+    const uint64_t b0 = hist[2 * lane], b1 = hist[2 * lane + 1];
+    __syncwarp();
+    const uint64_t run = b0 + b1;
+    uint64_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    const uint64_t base = x - run;
+    const uint64_t total = __shfl_sync(0xffffffffu, x, 31);
+    uint32_t dloc = 64;
+    uint64_t exloc = 0;
+    if (base + b0 + b1 > R) { dloc = 2 * lane + 1; exloc = base + b0; }
+    if (base + b0 > R) { dloc = 2 * lane; exloc = base; }
+    const uint32_t d = __reduce_min_sync(0xffffffffu, dloc);
+    if (d == 64) {
+      dsum += total;
+      out[0] = khi;
+      out[1] = 0;
+      out[2] = dsum;
+      return;
+    }
+    const uint64_t ex = __shfl_sync(0xffffffffu, exloc, (int)(d >> 1));
+    R -= ex;
+    dsum += ex;
+    const uint64_t nlo = klo + ((uint64_t)d << shift);
+    const uint64_t nhi_full = nlo + ((1ull << shift) - 1);
+    const uint64_t nhi = nhi_full < khi ? nhi_full : khi;
+    uint64_t mn = ~0ull, mx = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint64_t k = abs_bits(v[r]);
+      if (k >= nlo && k <= nhi) { mn = k < mn ? k : mn; mx = k > mx ? k : mx; }
+    }
+    klo = warp_min_u64(mn);
+    khi = warp_max_u64(mx);
+  }
+}
+
+struct Sel16 {
+  uint32_t mask;   // kept bits of this lane's 16 coefficients
+  uint64_t T;      // block total of lo energies
+  uint64_t hdisc;  // block hi-sum of the discarded set
+  int k;           // energy scale exponent (e = a^2 * 2^(2k))
+  bool nonfinite;
+};
+
+// v[r] = coefficient 16*lane + r of the warp's block.  scratch: 16 doubles per lane.
+__device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t eps_q, unsigned long long* hist,
+                                          double* scratch) {
+  Sel16 s{0u, 0ull, 0ull, 0, false};
+  uint32_t hm = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) hm = ::max(hm, (uint32_t)__double2hiint(v[r]) & 0x7fffffffu);
+  hm = __reduce_max_sync(0xffffffffu, hm);
+  if (hm >= 0x7ff00000u) { s.nonfinite = true; return s; }
+  int sexp;
+  if (hm >= 0x00100000u) {
+    sexp = (int)(hm >> 20) - 1022;
+  } else {  // subnormal maximum or all-zero block (rare)
+    uint64_t mb = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) { const uint64_t b = abs_bits(v[r]); mb = b > mb ? b : mb; }
+    mb = warp_max_u64(mb);
+    if (mb == 0) return s;  // all-zero block keeps nothing
+    sexp = 64 - __clzll((long long)mb) - 1074;
+  }
+  constexpr int K = energy_K(8);
+  int k = K - sexp;
+  s.k = k;
+  const bool tiny = k > 1023;  // |a| < 2^-998: exact pre-scale by 2^(k-1023)
+  if (tiny) {
+    const double pre = pow2d(k - 1023);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = __dmul_rn(v[r], pre);
+    k = 1023;
+  }
+  const double f = pow2d(k);
+  uint64_t lo[16];
+  uint64_t t0 = 0, t1 = 0;
+#pragma unroll
+  for (int r = 0; r < 16; r += 2) {
+    lo[r] = e_lo(v[r], f);
+    lo[r + 1] = e_lo(v[r + 1], f);
+    t0 += lo[r];
+    t1 += lo[r + 1];
+  }
+  const uint64_t T = warp_sum_u58(t0 + t1);
+  s.T = T;
+  const uint64_t thr = __umul64hi(T, eps_q);
+  uint32_t mH = 0;
+  uint64_t n0 = 0, n1 = 0;
+#pragma unroll
+  for (int r = 0; r < 16; r += 2) {
+    const uint64_t ha = lo[r] + (abs_bits(v[r]) != 0 ? 1ull : 0ull);
+    const uint64_t hb = lo[r + 1] + (abs_bits(v[r + 1]) != 0 ? 1ull : 0ull);
+    if (ha > thr) mH |= 1u << r; else n0 += ha;
+    if (hb > thr) mH |= 1u << (r + 1); else n1 += hb;
+  }
+  const uint64_t SN = warp_sum_u58(n0 + n1);
+  if (SN <= thr) {
+    s.mask = mH;
+    s.hdisc = SN;
+  } else {
+    // One-move path: the last element of the non-kept prefix (largest |a|, smallest
+    // index among ties) joins the kept set if that suffices.
+    uint64_t mk = 0;
+    int mi = 16;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint64_t kk = ((mH >> r) & 1u) ? 0ull : abs_bits(v[r]);
+      if (kk > mk) { mk = kk; mi = r; }
+    }
+    const uint64_t gmk = warp_max_u64(mk);
+    const uint32_t cand = (mk == gmk && mi < 16) ? (uint32_t)(16 * lane + mi) : 0xffffu;
+    const uint32_t gidx = __reduce_min_sync(0xffffffffu, cand);
+    const uint64_t h1 = gmk ? e_lo(__longlong_as_double((long long)gmk), f) + 1ull : 0ull;
+    if (gmk != 0 && SN - h1 <= thr) {
+      s.mask = mH | (((int)(gidx >> 4) == lane) ? (1u << (gidx & 15)) : 0u);
+      s.hdisc = SN - h1;
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) scratch[r] = v[r];
+      uint64_t res[3];
+      radix_select16(scratch, lane, thr, f, hist, res);
+      const uint64_t tstar = res[0];
+      const uint32_t icut = (uint32_t)res[1];
+      uint32_t mk2 = 0;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint64_t kk = abs_bits(v[r]);
+        const uint32_t j = (uint32_t)(16 * lane + r);
+        if (kk > tstar || (kk == tstar && j < icut)) mk2 |= 1u << r;
+      }
+      s.mask = mk2;
+      s.hdisc = res[2];
+    }
+  }
+  if (tiny) {
+    const double un = pow2d(1023 - s.k);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = __dmul_rn(v[r], un);
+  }
+  return s;
+}
+
+// --------------------------- compress ---------------------------------------
+constexpr int kC8WarpBytes = kF8Stages * 4096 + 512 + 128;  // stages | hist | mbarriers
+constexpr int kC8Smem = kF8Warps * kC8WarpBytes;
+
+__global__ void __launch_bounds__(kF8Warps * 32) compress8_kernel(CompressArgs A) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* wbase = smem + warp * kC8WarpBytes;
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(wbase + kF8Stages * 4096);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kF8Stages * 4096 + 512);
+  const int kzp = lane >> 2, qp = lane & 3;  // y-line / x-line roles
+  uint32_t* counts = reinterpret_cast<uint32_t*>(A.stream);
+  uint16_t* masks16 = reinterpret_cast<uint16_t*>(A.stream + A.mask_off);
+  const uint64_t W = (uint64_t)gridDim.x * kF8Warps;
+  const uint64_t gw = (uint64_t)blockIdx.x * kF8Warps + warp;
+  const uint64_t B = A.nblocks;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kF8Stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](uint64_t blk, int st) {
+    if (lane == 0 && blk < B) {
+      mbar_arrive_tx(&bars[st], 4096u);
+      bulk_g2s_evict_first(wbase + st * 4096, A.field + blk * 512, 4096u, &bars[st]);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < kF8Stages; ++s) issue(gw + s * W, s);
+  double tot_acc = 0.0, disc_acc = 0.0;
+  double scratch[16];
+  int st = 0;
+  uint32_t ph = 0;
+  for (uint64_t blk = gw; blk < B; blk += W) {
+    double2* sb = reinterpret_cast<double2*>(wbase + st * 4096);
+    mbar_wait(&bars[st], (ph >> st) & 1u);
+    ph ^= 1u << st;
+    double v[16];
+#pragma unroll
+    for (int z = 0; z < 8; ++z) {
+      const double2 t = sb[z * 32 + lane];
+      v[2 * z] = t.x;
+      v[2 * z + 1] = t.y;
+    }
+    __syncwarp();
+    lines<8, 2, 0, 1, 2, false>(v);  // z sweep
+#pragma unroll
+    for (int kz = 0; kz < 8; ++kz) sb[kz * 32 + swz(kz, lane)] = make_double2(v[2 * kz], v[2 * kz + 1]);
+    __syncwarp();
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const double2 t = sb[kzp * 32 + swz(kzp, y * 4 + qp)];
+      v[2 * y] = t.x;
+      v[2 * y + 1] = t.y;
+    }
+    __syncwarp();
+    lines<8, 2, 0, 1, 2, false>(v);  // y sweep
+#pragma unroll
+    for (int ky = 0; ky < 8; ++ky) sb[kzp * 32 + swz(kzp, ky * 4 + qp)] = make_double2(v[2 * ky], v[2 * ky + 1]);
+    __syncwarp();
+#pragma unroll
+    for (int kyi = 0; kyi < 2; ++kyi)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 t = sb[kzp * 32 + swz(kzp, (2 * qp + kyi) * 4 + q)];
+        v[kyi * 8 + 2 * q] = t.x;
+        v[kyi * 8 + 2 * q + 1] = t.y;
+      }
+    fence_proxy_async();
+    __syncwarp();
+    issue(blk + kF8Stages * W, st);  // refill this stage
+    st = (st + 1 == kF8Stages) ? 0 : st + 1;
+    lines<8, 1, 0, 8, 2, false>(v);  // x sweep: v[r] = coefficient 16*lane + r
+    const Sel16 sel = select16(v, lane, A.eps_q, hist, scratch);
+    if (sel.nonfinite && lane == 0) atomicOr(A.ws.flags, kFlagNonFinite);
+    const uint32_t mask = sel.nonfinite ? 0u : sel.mask;
+    const uint32_t nk = (uint32_t)__popc(mask);
+    const uint32_t off = warp_exscan_u32(nk, lane);
+    const uint32_t kept = __shfl_sync(0xffffffffu, off + nk, 31);
+    if (lane == 0) {
+      counts[blk] = kept;
+      if (blk + 1 == B)
+        for (uint64_t pb = B; pb < ((B + 3) & ~3ull); ++pb) counts[pb] = 0;  // pad to 16 B
+    }
+    masks16[blk * 32 + lane] = (uint16_t)mask;
+    double* dst = A.vslot + blk * 512 + off;
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if ((mask >> r) & 1u) *dst++ = v[r];
+    if (!sel.nonfinite && sel.T) {
+      tot_acc += ldexp((double)sel.T, -2 * sel.k);
+      disc_acc += ldexp((double)sel.hdisc, -2 * sel.k);
+    }
+  }
+  if (lane == 0) {
+    A.ws.partials[gw * 4 + 0] = tot_acc;
+    A.ws.partials[gw * 4 + 1] = disc_acc;
+  }
+}
+
+// --------------------------- block offsets / compact passes -----------------
+// off[b] = sum of counts of blocks < b (exclusive), off[B] = total.  CTA chunks of
+// 256 blocks chained by a decoupled look-back on ws.status with a dynamic chunk
+// claim (deadlock free).  With vslot != nullptr (compress) every block's kept
+// values are then moved from its fixed slot into the packed value region.
+constexpr int kOffThreads = 256;
+
+__global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8_t* stream, uint64_t nblocks,
+                                                                    uint64_t* off, Workspace ws,
+                                                                    const double* vslot, double* vals,
+                                                                    uint64_t cap_vals) {
+  __shared__ uint64_t wsum[kOffThreads / 32];
+  __shared__ uint64_t s_prefix;
+  __shared__ uint32_t s_chunk;
+  __shared__ uint64_t s_off[kOffThreads + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t* counts = reinterpret_cast<const uint32_t*>(stream);
+  const uint32_t nchunks = (uint32_t)((nblocks + kOffThreads - 1) / kOffThreads);
+  for (;;) {
+    if (tid == 0) {
+      const uint32_t c = atomicAdd(ws.counter, 1u);
+      if (c == nchunks + ws.total_warps - 1) *ws.counter = 0;
+      s_chunk = c;
+    }
+    __syncthreads();
+    const uint32_t chunk = s_chunk;
+    if (chunk >= nchunks) break;
+    const uint64_t b = (uint64_t)chunk * kOffThreads + tid;
+    const uint64_t v = b < nblocks ? (uint64_t)counts[b] : 0ull;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint64_t wex = 0, agg = 0;
+#pragma unroll
+    for (int w = 0; w < kOffThreads / 32; ++w) {
+      wex += (w < warp) ? wsum[w] : 0ull;
+      agg += wsum[w];
+    }
+    if (warp == 0) {
+      const uint64_t pre = warp_lookback(ws.status, chunk, agg, ws.epoch);
+      if (lane == 0) s_prefix = pre;
+    }
+    __syncthreads();
+    const uint64_t excl = s_prefix + wex + x - v;
+    s_off[tid] = excl;
+    if (tid == kOffThreads - 1) s_off[kOffThreads] = excl + v;
+    if (b < nblocks) off[b] = excl;
+    if (b + 1 == nblocks) {
+      off[nblocks] = excl + v;
+      if (vslot && excl + v > cap_vals) atomicOr(ws.flags, kFlagOverflow);
+    }
+    __syncthreads();
+    if (vslot) {
+      for (int t = warp; t < kOffThreads; t += kOffThreads / 32) {
+        const uint64_t bb = (uint64_t)chunk * kOffThreads + t;
+        if (bb >= nblocks) break;
+        const uint64_t o0 = s_off[t], n = s_off[t + 1] - o0;
+        if (o0 + n > cap_vals) continue;
+        const double* src = vslot + bb * 512;
+        for (uint64_t i = lane; i < n; i += 32) vals[o0 + i] = src[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// --------------------------- decompress -------------------------------------
+// stage: [0,16) the 16-B aligned counts quad | [16,80) mask | [96, ...) values
+constexpr int kD8Stage = 96 + 4096 + 32;
+constexpr int kD8StageBytes = (kD8Stage + 127) & ~127;
+constexpr int kD8WarpBytes = kF8Stages * kD8StageBytes + 128;
+constexpr int kD8Smem = kF8Warps * kD8WarpBytes;
+
+struct Decompress8Args {
+  DecompressArgs d;
+  const uint64_t* off;  // block value offsets (block_offsets8_kernel), off[B] = total
+};
+
+__global__ void __launch_bounds__(kF8Warps * 32) decompress8_kernel(Decompress8Args P) {
+  const DecompressArgs& A = P.d;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* wbase = smem + warp * kD8WarpBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kF8Stages * kD8StageBytes);
+  const int kzp = lane >> 2, qp = lane & 3;
+  const int q = lane & 3, y = lane >> 2;
+  const uint64_t W = (uint64_t)gridDim.x * kF8Warps;
+  const uint64_t gw = (uint64_t)blockIdx.x * kF8Warps + warp;
+  const uint64_t B = A.nblocks;
+  const uint64_t sb_floor16 = A.stream_bytes & ~15ull;
+  const double wxy0 = __dmul_rn(Wg<8>(2 * q), Wg<8>(y));
+  const double wxy1 = __dmul_rn(Wg<8>(2 * q + 1), Wg<8>(y));
+  double e2 = 0.0, n2 = 0.0;
+  uint64_t einf = 0, uinf = 0;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kF8Stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  auto issue = [&](uint64_t blk, int st, uint64_t o0, uint64_t o1) {
+    if (lane == 0 && blk < B) {
+      unsigned char* sp = wbase + st * kD8StageBytes;
+      const uint64_t a0 = (A.val_off + 8 * o0) & ~15ull;
+      uint64_t a1 = (A.val_off + 8 * o1 + 15) & ~15ull;
+      if (a1 > sb_floor16) a1 = sb_floor16;
+      const uint32_t vbytes = (a1 > a0 && o1 - o0 <= 512) ? (uint32_t)(a1 - a0) : 0u;
+      mbar_arrive_tx(&bars[st], 16u + 64u + vbytes);
+      bulk_g2s(sp, A.stream + ((4 * blk) & ~15ull), 16u, &bars[st]);
+      bulk_g2s(sp + 16, A.stream + A.mask_off + 64 * blk, 64u, &bars[st]);
+      if (vbytes) bulk_g2s(sp + 96, A.stream + a0, vbytes, &bars[st]);
+    }
+  };
+  static_assert(kF8Stages == 2, "offset pipeline assumes two stages");
+  // offsets of the current block and the next one (loaded one iteration ahead)
+  uint64_t o0 = 0, o1 = 0, p0 = 0, p1 = 0;
+  if (gw < B) { o0 = P.off[gw]; o1 = P.off[gw + 1]; }
+  if (gw + W < B) { p0 = P.off[gw + W]; p1 = P.off[gw + W + 1]; }
+  issue(gw, 0, o0, o1);
+  issue(gw + W, 1, p0, p1);
+  int st = 0;
+  uint32_t ph = 0;
+  for (uint64_t blk = gw; blk < B; blk += W) {
+    unsigned char* sp = wbase + st * kD8StageBytes;
+    uint64_t r0 = 0, r1 = 0;  // offsets of blk + 2W, consumed by the refill below
+    if (blk + 2 * W < B) { r0 = P.off[blk + 2 * W]; r1 = P.off[blk + 2 * W + 1]; }
+    mbar_wait(&bars[st], (ph >> st) & 1u);
+    ph ^= 1u << st;
+    const uint32_t cnt = reinterpret_cast<const uint32_t*>(sp)[blk & 3];
+    uint32_t m = reinterpret_cast<const uint16_t*>(sp + 16)[lane];
+    const uint32_t pc = (uint32_t)__popc(m);
+    const uint32_t inoff = warp_exscan_u32(pc, lane);
+    const uint32_t tot = __shfl_sync(0xffffffffu, inoff + pc, 31);
+    const bool ok = tot == cnt && o1 - o0 == cnt && A.val_off + 8 * o1 <= A.stream_bytes;
+    if (!ok) {
+      if (lane == 0) atomicOr(A.ws.flags, kFlagShape);
+      m = 0;
+    }
+    double v[16];
+    {
+      const double* sv = reinterpret_cast<const double*>(sp + 96) + (((A.val_off + 8 * o0) & 15ull) >> 3) + inoff;
+      int o = 0;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = ((m >> r) & 1u) ? sv[o++] : 0.0;
+      // the final 8 bytes of a stream whose length is 8 mod 16 are not in the bulk copy
+      if (m && A.val_off + 8 * o1 > sb_floor16) {
+        const uint64_t last = (A.stream_bytes - A.val_off) / 8 - 1;
+        const uint64_t first = o0 + inoff;
+        int oo = 0;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if ((m >> r) & 1u) {
+            if (first + oo == last) v[r] = reinterpret_cast<const double*>(A.stream + A.val_off)[last];
+            ++oo;
+          }
+      }
+    }
+    __syncwarp();
+    double2* sb = reinterpret_cast<double2*>(sp);
+    lines<8, 1, 0, 8, 2, true>(v);  // inverse x sweep
+#pragma unroll
+    for (int kyi = 0; kyi < 2; ++kyi)
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq)
+        sb[kzp * 32 + swz(kzp, (2 * qp + kyi) * 4 + qq)] = make_double2(v[kyi * 8 + 2 * qq], v[kyi * 8 + 2 * qq + 1]);
+    __syncwarp();
+#pragma unroll
+    for (int ky = 0; ky < 8; ++ky) {
+      const double2 t = sb[kzp * 32 + swz(kzp, ky * 4 + qp)];
+      v[2 * ky] = t.x;
+      v[2 * ky + 1] = t.y;
+    }
+    __syncwarp();
+    lines<8, 2, 0, 1, 2, true>(v);  // inverse y sweep
+#pragma unroll
+    for (int yy = 0; yy < 8; ++yy) sb[kzp * 32 + swz(kzp, yy * 4 + qp)] = make_double2(v[2 * yy], v[2 * yy + 1]);
+    __syncwarp();
+#pragma unroll
+    for (int z = 0; z < 8; ++z) {
+      const double2 t = sb[z * 32 + swz(z, lane)];
+      v[2 * z] = t.x;
+      v[2 * z + 1] = t.y;
+    }
+    fence_proxy_async();
+    __syncwarp();
+    issue(blk + 2 * W, st, r0, r1);
+    st ^= 1;
+    o0 = p0; o1 = p1;
+    p0 = r0; p1 = r1;
+    lines<8, 2, 0, 1, 2, true>(v);  // inverse z sweep
+    double2* dst = reinterpret_cast<double2*>(A.out + blk * 512) + lane;
+#pragma unroll
+    for (int z = 0; z < 8; ++z) stg_stream(dst + z * 32, make_double2(v[2 * z], v[2 * z + 1]));
+    if (A.orig) {
+      const double2* src = reinterpret_cast<const double2*>(A.orig + blk * 512) + lane;
+#pragma unroll
+      for (int z = 0; z < 8; ++z) {
+        const double2 o = ldg_stream(src + z * 32);
+        const double wz = Wg<8>(z);
+        const double w0 = __dmul_rn(wxy0, wz), w1 = __dmul_rn(wxy1, wz);
+        const double da = __dsub_rn(o.x, v[2 * z]), db = __dsub_rn(o.y, v[2 * z + 1]);
+        e2 = __fma_rn(__dmul_rn(w0, da), da, e2);
+        e2 = __fma_rn(__dmul_rn(w1, db), db, e2);
+        n2 = __fma_rn(__dmul_rn(w0, o.x), o.x, n2);
+        n2 = __fma_rn(__dmul_rn(w1, o.y), o.y, n2);
+        uint64_t t;
+        t = abs_bits(da); einf = t > einf ? t : einf;
+        t = abs_bits(db); einf = t > einf ? t : einf;
+        t = abs_bits(o.x); uinf = t > uinf ? t : uinf;
+        t = abs_bits(o.y); uinf = t > uinf ? t : uinf;
+      }
+    }
+  }
+  if (A.orig) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      e2 = __dadd_rn(e2, __shfl_xor_sync(0xffffffffu, e2, o));
+      n2 = __dadd_rn(n2, __shfl_xor_sync(0xffffffffu, n2, o));
+      uint64_t t = __shfl_xor_sync(0xffffffffu, einf, o); einf = t > einf ? t : einf;
+      t = __shfl_xor_sync(0xffffffffu, uinf, o); uinf = t > uinf ? t : uinf;
+    }
+    if (lane == 0) {
+      A.ws.partials[gw * 4 + 0] = e2;
+      A.ws.partials[gw * 4 + 1] = n2;
+      A.ws.partials[gw * 4 + 2] = __longlong_as_double((long long)einf);
+      A.ws.partials[gw * 4 + 3] = __longlong_as_double((long long)uinf);
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace isf

@@ -13,7 +13,7 @@
 #include <string>
 
 #include "../../include/isf_lossy.h"
-#include "dlt_kernels.cuh"
+#include "dlt_fast8.cuh"
 
 using namespace isf::dev;
 
@@ -136,7 +136,7 @@ struct DeviceGuard {
 
 uint64_t header_bytes(uint32_t P, uint64_t nblocks) {
   const uint64_t W = ((uint64_t)P * P * P + 63) / 64;
-  return ((4 * nblocks + 7) & ~7ull) + 8 * W * nblocks;
+  return ((4 * nblocks + 15) & ~15ull) + 8 * W * nblocks;
 }
 
 }  // namespace
@@ -149,6 +149,10 @@ struct isf_lossy_plan {
   size_t status_cap = 0;
   double* partials = nullptr;
   size_t partials_cap = 0;  // slots of 4 doubles
+  uint64_t* toff = nullptr;  // tile offsets (lx = 8 fast path)
+  size_t toff_cap = 0;
+  double* vslot = nullptr;   // compress value slots (lx = 8 fast path)
+  size_t vslot_cap = 0;
   uint32_t* counter = nullptr;
   unsigned long long* flags = nullptr;
   isf_lossy_stats* d_stats = nullptr;
@@ -170,13 +174,20 @@ struct isf_lossy_plan {
 
 namespace {
 
-int ensure(isf_lossy_plan* p, size_t ntiles, size_t nparts) {
+// ntiles: look-back descriptors; nparts: partial slots; noff: block-offset entries
+int ensure(isf_lossy_plan* p, size_t ntiles, size_t nparts, size_t noff) {
   if (ntiles > p->status_cap) {
     if (p->status) cudaFree(p->status);
     size_t cap = std::max<size_t>(ntiles, 1024);
     CUDA_TRY(cudaMalloc(&p->status, cap * sizeof(uint64_t)));
     CUDA_TRY(cudaMemset(p->status, 0, cap * sizeof(uint64_t)));
     p->status_cap = cap;
+  }
+  if (noff > p->toff_cap) {
+    if (p->toff) cudaFree(p->toff);
+    size_t cap = std::max<size_t>(noff, 1024);
+    CUDA_TRY(cudaMalloc(&p->toff, cap * sizeof(uint64_t)));
+    p->toff_cap = cap;
   }
   if (nparts > p->partials_cap) {
     if (p->partials) cudaFree(p->partials);
@@ -323,15 +334,15 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
   CUDA_TRY(cudaMallocHost(&p->h_stats, sizeof(isf_lossy_stats)));
   build_operators((int)P, p->F, p->B, p->x, p->w);
   if (use_fast8(p)) {
-    CUDA_TRY(cudaFuncSetAttribute(compress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarps8 * kWarpBytes8));
-    CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarps8 * kWarpBytesD8));
+    CUDA_TRY(cudaFuncSetAttribute(compress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
+    CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kD8Smem));
     int occ = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel, kWarps8 * 32, kWarps8 * kWarpBytes8));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel, kF8Warps * 32, kC8Smem));
     p->grid8c = p->sms * std::max(occ, 1);
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel, kWarps8 * 32, kWarps8 * kWarpBytesD8));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel, kF8Warps * 32, kD8Smem));
     p->grid8d = p->sms * std::max(occ, 1);
   }
-  CUDA_TRY(ensure(p, 1 << 16, 1 << 14) == 0 ? cudaSuccess : cudaErrorMemoryAllocation);
+  CUDA_TRY(ensure(p, 1 << 16, 1 << 14, 1 << 16) == 0 ? cudaSuccess : cudaErrorMemoryAllocation);
   *out = p;
   return 0;
 }
@@ -341,6 +352,8 @@ int isf_lossy_plan_destroy(isf_lossy_plan* p) {
   DeviceGuard dg(p->device);
   cudaFree(p->status);
   cudaFree(p->partials);
+  cudaFree(p->toff);
+  cudaFree(p->vslot);
   cudaFree(p->counter);
   cudaFree(p->flags);
   cudaFree(p->d_stats);
@@ -384,33 +397,57 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   DeviceGuard dg(p->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
   const bool fast = use_fast8(p);
-  const uint64_t ntiles64 = fast ? (B + 3) / 4 : B;
-  if (ntiles64 >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
-  const uint32_t ntiles = (uint32_t)ntiles64;
-  if (int rc = ensure(p, ntiles, ntiles)) return rc;
+  if (B >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
+  const uint32_t ntiles = (uint32_t)B;  // generic: one tile per block; fast: one warp per block
+  const uint32_t nchunks = (ntiles + kOffThreads - 1) / kOffThreads;
+  const size_t nparts = fast ? (size_t)p->grid8c * kF8Warps : (size_t)ntiles;
+  if (int rc = ensure(p, fast ? nchunks : ntiles, nparts, fast ? B + 1 : 0)) return rc;
   CompressArgs a;
   a.field = d_field;
   a.nblocks = B;
   a.comps = (int)p->comps;
   a.stream = (uint8_t*)d_stream;
   a.cap = capacity;
-  a.mask_off = (4 * B + 7) & ~7ull;
+  a.mask_off = (4 * B + 15) & ~15ull;
   a.val_off = hdr;
   a.eps_q = eps_q_of(max_error);
+  a.vslot = nullptr;
   a.ws = Workspace{p->status, p->partials, p->counter, p->flags, next_epoch(p, s), ntiles, 0};
+  const uint64_t* total_ptr = nullptr;
+  int launches = 2;
+  uint64_t parts = ntiles;
   if (fast) {
-    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8c, (ntiles + kWarps8 - 1) / kWarps8);
-    a.ws.total_warps = grid * kWarps8;
-    compress8_kernel<<<grid, kWarps8 * 32, kWarps8 * kWarpBytes8, s>>>(a);
+    const size_t slot_bytes = (size_t)B * 512 * sizeof(double);
+    if (slot_bytes > p->vslot_cap) {
+      if (p->vslot) cudaFree(p->vslot);
+      p->vslot = nullptr;
+      p->vslot_cap = 0;
+      CUDA_TRY(cudaMalloc(&p->vslot, slot_bytes));
+      p->vslot_cap = slot_bytes;
+    }
+    a.vslot = p->vslot;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8c, (B + kF8Warps - 1) / kF8Warps);
+    a.ws.total_warps = grid * kF8Warps;
+    compress8_kernel<<<grid, kF8Warps * 32, kC8Smem, s>>>(a);
     CUDA_TRY(cudaGetLastError());
+    parts = (uint64_t)grid * kF8Warps;
+    Workspace wo = a.ws;
+    wo.ntiles = nchunks;
+    wo.total_warps = std::min<uint32_t>(nchunks, (uint32_t)p->sms * 4);
+    block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>(
+        a.stream, B, p->toff, wo, p->vslot, reinterpret_cast<double*>(a.stream + a.val_off),
+        capacity > hdr ? (capacity - hdr) / 8 : 0);
+    CUDA_TRY(cudaGetLastError());
+    total_ptr = p->toff + B;
+    launches = 3;
   } else {
     if (int rc = dispatch_compress_generic(AllLx{}, (int)p->P, p, a, s)) return rc;
   }
-  FinalizeArgs f{0, p->partials, ntiles, p->status, ntiles, p->flags, d_stats, B,
+  FinalizeArgs f{0, p->partials, parts, p->status, total_ptr, ntiles, p->flags, d_stats, B,
                  B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
   finalize_kernel<<<1, kFinThreads, 0, s>>>(f);
   CUDA_TRY(cudaGetLastError());
-  p->last_launches = 2;
+  p->last_launches = launches;
   return 0;
 }
 
@@ -454,37 +491,48 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
   DeviceGuard dg(p->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
   const bool fast = use_fast8(p);
-  const uint64_t ntiles64 = fast ? (B + 3) / 4 : B;
-  if (ntiles64 >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
-  const uint32_t ntiles = (uint32_t)ntiles64;
-  const size_t nparts = fast ? (size_t)p->grid8d * kWarps8 : (size_t)p->sms * 16;
-  if (int rc = ensure(p, ntiles, nparts)) return rc;
+  if (B >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
+  const uint32_t ntiles = (uint32_t)B;
+  const uint32_t nchunks = (ntiles + kOffThreads - 1) / kOffThreads;
+  const size_t nparts = fast ? (size_t)p->grid8d * kF8Warps : (size_t)p->sms * 16;
+  if (int rc = ensure(p, fast ? nchunks : ntiles, nparts, fast ? B + 1 : 0)) return rc;
   DecompressArgs a;
   a.stream = (const uint8_t*)d_stream;
   a.stream_bytes = stream_bytes;
   a.nblocks = B;
   a.comps = (int)p->comps;
-  a.mask_off = (4 * B + 7) & ~7ull;
+  a.mask_off = (4 * B + 15) & ~15ull;
   a.val_off = hdr;
   a.out = d_out;
   a.orig = d_original;
   a.ws = Workspace{p->status, p->partials, p->counter, p->flags, next_epoch(p, s), ntiles, 0};
   uint32_t grid = 0, parts = 0;
+  const uint64_t* total_ptr = nullptr;
+  int launches = 2;
   if (fast) {
-    grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8d, (ntiles + kWarps8 - 1) / kWarps8);
-    a.ws.total_warps = grid * kWarps8;
-    decompress8_kernel<<<grid, kWarps8 * 32, kWarps8 * kWarpBytesD8, s>>>(a);
+    Workspace wo = a.ws;
+    wo.ntiles = nchunks;
+    wo.total_warps = std::min<uint32_t>(nchunks, (uint32_t)p->sms * 4);
+    block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>((const uint8_t*)d_stream, B, p->toff, wo,
+                                                                 nullptr, nullptr, 0);
     CUDA_TRY(cudaGetLastError());
-    parts = grid * kWarps8;
+    grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8d, (B + kF8Warps - 1) / kF8Warps);
+    a.ws.total_warps = grid * kF8Warps;
+    Decompress8Args a8{a, p->toff};
+    decompress8_kernel<<<grid, kF8Warps * 32, kD8Smem, s>>>(a8);
+    CUDA_TRY(cudaGetLastError());
+    parts = grid * kF8Warps;
+    total_ptr = p->toff + B;
+    launches = 3;
   } else {
     if (int rc = dispatch_decompress_generic(AllLx{}, (int)p->P, p, a, s, &grid)) return rc;
     parts = grid;
   }
-  FinalizeArgs f{1, p->partials, d_original ? parts : 0u, p->status, ntiles, p->flags, d_stats, B,
+  FinalizeArgs f{1, p->partials, d_original ? parts : 0u, p->status, total_ptr, ntiles, p->flags, d_stats, B,
                  B * (uint64_t)p->P * p->P * p->P * 8, hdr, d_original ? 1 : 0};
   finalize_kernel<<<1, kFinThreads, 0, s>>>(f);
   CUDA_TRY(cudaGetLastError());
-  p->last_launches = 2;
+  p->last_launches = launches;
   return 0;
 }
 
@@ -666,7 +714,7 @@ __global__ void spectral_stream_kernel(uint8_t* stream, uint64_t nblocks, uint64
     vals[t] = __dmul_rn(U2, amp[j]);
     if (j == 0) {
       counts[b] = (uint32_t)n3;
-      if (b + 1 == nblocks && (nblocks & 1)) counts[b + 1] = 0;
+      if (b + 1 == nblocks) for (uint64_t pb = nblocks; pb < ((nblocks + 3) & ~3ull); ++pb) counts[pb] = 0;
     }
     if (j < (uint32_t)W) masks[b * W + j] = (j == (uint32_t)W - 1) ? lastmask : ~0ull;
   }
@@ -701,7 +749,7 @@ int isf_lossy_generate_spectral(isf_lossy_plan* p, double* d_out, uint64_t block
   CUDA_TRY(cudaMallocAsync(&tmp, bytes, s));
   CUDA_TRY(cudaMallocAsync((void**)&d_amp, sizeof(double) * n3, s));
   CUDA_TRY(cudaMemcpyAsync(d_amp, h_amp, sizeof(double) * n3, cudaMemcpyHostToDevice, s));
-  spectral_stream_kernel<<<p->sms * 8, 256, 0, s>>>((uint8_t*)tmp, nblocks, block0, n3, W, (4 * nblocks + 7) & ~7ull,
+  spectral_stream_kernel<<<p->sms * 8, 256, 0, s>>>((uint8_t*)tmp, nblocks, block0, n3, W, (4 * nblocks + 15) & ~15ull,
                                                      header_bytes(p->P, nblocks), seed, d_amp);
   CUDA_TRY(cudaGetLastError());
   int rc = isf_lossy_decompress(p, tmp, bytes, nblocks, d_out, nullptr, nullptr, cuda_stream);

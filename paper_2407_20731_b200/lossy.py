@@ -191,7 +191,7 @@ class CompressedBlock:
         B = self.nblocks
         W = (P ** 3 + 63) // 64
         s = self.stream
-        m0 = (4 * B + 7) & ~7
+        m0 = (4 * B + 15) & ~15
         counts = s[: 4 * B].view(torch.int32)
         masks = s[m0: m0 + 8 * W * B].view(torch.int64).reshape(B, W)
         vals = s[m0 + 8 * W * B:].view(torch.float64)
@@ -214,7 +214,7 @@ class CompressedBlock:
         P3 = self.points_per_element_axis ** 3
         B = self.nblocks
         W = (P3 + 63) // 64
-        m0 = (4 * B + 7) & ~7
+        m0 = (4 * B + 15) & ~15
         counts = host[: 4 * B].view(np.uint32)
         masks = host[m0: m0 + 8 * W * B].view(np.uint64).reshape(B, W)
         vals = host[m0 + 8 * W * B:].view(np.float64)
