@@ -10,6 +10,7 @@
 #include "isf_oracle.h"
 
 #include <math.h>
+#include <quadmath.h>
 #include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
@@ -22,46 +23,47 @@
 
 /* ------------------------------------------------------------------------- */
 /* GLL nodes / weights / Legendre matrices.               */
-/* Nodes: +-1 and the roots of P'_N (N = lx-1), Newton in long double on       */
-/* x P_N - P_{N-1} = 0 ... mirrored exactly x_{N-i} = -x_i.                    */
+/* Nodes: +-1 and the roots of P'_N (N = lx-1), Newton in binary128 on        */
+/* x P_N - P_{N-1} = 0, mirrored exactly x_{N-i} = -x_i.  binary128 makes the  */
+/* single rounding to binary64 correct (pinned by tests/golden, 40 digits).    */
 /* ------------------------------------------------------------------------- */
-static void legendre_all(int N, long double x, long double* P /* N+1 */) {
-    P[0] = 1.0L;
+typedef __float128 qreal;
+
+static void legendre_all(int N, qreal x, qreal* P /* N+1 */) {
+    P[0] = 1;
     if (N >= 1) P[1] = x;
-    for (int k = 2; k <= N; ++k)
-        P[k] = ((long double)(2 * k - 1) * x * P[k - 1] - (long double)(k - 1) * P[k - 2]) /
-               (long double)k;
+    for (int k = 2; k <= N; ++k) P[k] = ((qreal)(2 * k - 1) * x * P[k - 1] - (qreal)(k - 1) * P[k - 2]) / (qreal)k;
 }
 
-static void gll_ld(int lx, long double* x, long double* w) {
+static void gll_q(int lx, qreal* x, qreal* w) {
     const int N = lx - 1;
-    long double P[ISO_MAX_LX + 1];
+    qreal P[ISO_MAX_LX + 1];
     for (int i = 0; i <= N; ++i) {
-        /* Chebyshev-Gauss-Lobatto initial guess, ascending order */
-        long double xi = -cosl(3.14159265358979323846264338327950288L * (long double)i / (long double)N);
+        const qreal pi = acosq((qreal)-1);
+        qreal xi = -cosq(pi * (qreal)i / (qreal)N); /* Chebyshev-Gauss-Lobatto guess */
         for (int it = 0; it < 100; ++it) {
             legendre_all(N, xi, P);
-            long double dx = (xi * P[N] - P[N - 1]) / ((long double)(N + 1) * P[N]);
+            const qreal dx = (xi * P[N] - P[N - 1]) / ((qreal)(N + 1) * P[N]);
             xi -= dx;
-            if (fabsl(dx) < 1e-30L) break;
+            if (fabsq(dx) < (qreal)1e-33) break;
         }
         x[i] = xi;
     }
-    x[0] = -1.0L;
-    x[N] = 1.0L;
+    x[0] = -1;
+    x[N] = 1;
     for (int i = 0; i < lx / 2; ++i) x[N - i] = -x[i];
-    if (lx % 2) x[lx / 2] = 0.0L;
+    if (lx % 2) x[lx / 2] = 0;
     for (int i = 0; i <= N; ++i) {
         legendre_all(N, x[i], P);
-        w[i] = 2.0L / ((long double)N * (long double)(N + 1) * P[N] * P[N]);
+        w[i] = (qreal)2 / ((qreal)N * (qreal)(N + 1) * P[N] * P[N]);
     }
     for (int i = 0; i < lx / 2; ++i) w[N - i] = w[i];
 }
 
 int iso_gll(int lx, double* x, double* w) {
     if (lx < 2 || lx > ISO_MAX_LX) return ERR_INVALID;
-    long double xl[ISO_MAX_LX], wl[ISO_MAX_LX];
-    gll_ld(lx, xl, wl);
+    qreal xl[ISO_MAX_LX], wl[ISO_MAX_LX];
+    gll_q(lx, xl, wl);
     for (int i = 0; i < lx; ++i) {
         x[i] = (double)xl[i];
         w[i] = (double)wl[i];
@@ -76,13 +78,13 @@ int iso_gll(int lx, double* x, double* w) {
 int iso_matrices(int lx, double* F, double* B) {
     if (lx < 2 || lx > ISO_MAX_LX) return ERR_INVALID;
     const int N = lx - 1;
-    long double x[ISO_MAX_LX], w[ISO_MAX_LX], P[ISO_MAX_LX + 1];
-    gll_ld(lx, x, w);
+    qreal x[ISO_MAX_LX], w[ISO_MAX_LX], P[ISO_MAX_LX + 1];
+    gll_q(lx, x, w);
     for (int i = 0; i < (lx + 1) / 2; ++i) {
         legendre_all(N, x[i], P);
         for (int k = 0; k < lx; ++k) {
-            long double g = (k < N) ? 2.0L / (long double)(2 * k + 1) : 2.0L / (long double)N;
-            long double rs = 1.0L / sqrtl(g);
+            const qreal g = (k < N) ? (qreal)2 / (qreal)(2 * k + 1) : (qreal)2 / (qreal)N;
+            const qreal rs = 1 / sqrtq(g);
             double f = (double)(w[i] * P[k] * rs);
             double b = (double)(P[k] * rs);
             if ((lx % 2) && i == lx / 2 && (k % 2)) { f = 0.0; b = 0.0; }
@@ -190,7 +192,7 @@ void iso_inv_block(int lx, const double* B, const double* a, double* u) {
 /*   s      = frexp exponent of max|a|   (2^(s-1) <= max|a| < 2^s)            */
 /*   a''_j  = |a_j| * 2^(K-s)            (exact whenever the result is >= 1)  */
 /*   e_j    = fl(a''_j * a''_j)  in [0, 2^50)                                 */
-/*   lo_j   = floor(e_j), hi_j = lo_j + (a_j != 0)   (integers, u64)          */
+/*   lo_j   = floor(e_j), hi_j = lo_j + 1  (integers, u64; hi_j > e_j)        */
 /*   T      = sum lo_j,  q = floor(fl(eps*eps) * 2^64),  thr = floor(T*q/2^64) */
 /*   discard order: |a| ascending, ties by index descending (= sort by |c|    */
 /*   descending, index ascending, read from the end)                         */
@@ -266,7 +268,7 @@ static uint32_t select_impl(int lx, const double* a, double max_error, double re
         double as = ldexp(fabs(a[j]), k);
         double e = as * as;
         lo[j] = (uint64_t)floor(e);
-        hi[j] = lo[j] + (a[j] != 0.0); /* upper bound of e; exact zeros cost nothing */
+        hi[j] = lo[j] + 1; /* strict upper bound of e: the discarded energy is never underestimated */
         T += lo[j];
         uint64_t b;
         memcpy(&b, &a[j], 8);

@@ -6,7 +6,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "isf_lossy.cu")
+SRC = [os.path.join(HERE, "csrc", "isf_lossy.cu"), os.path.join(HERE, "csrc", "gll_host.cpp")]
 OUT = os.path.join(HERE, "libisf_lossy.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -30,7 +30,7 @@ def needs_build() -> bool:
 def build(force: bool = False, log: str | None = None) -> str:
     if not force and not needs_build():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT, SRC, "-ldl"]
+    cmd = [NVCC, *FLAGS, "-o", OUT, *SRC, "-ldl", "-lquadmath"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if log:
         with open(log, "w") as f:

@@ -111,7 +111,7 @@ __device__ __forceinline__ void inv_line_ptr(double* p, int stride) {
 
 // ---------------------------------------------------------------------------
 // Energy quantisation: e = fl((|a|*2^k)^2) < 2^50,
-// lo = floor(e) via a round-down add of 2^52, hi = lo + (a != 0).
+// lo = floor(e) via a round-down add of 2^52, hi = lo + 1.
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int ceil_log2(int v) {
   int r = 0;
@@ -134,9 +134,11 @@ __device__ __forceinline__ uint64_t e_lo(double a, double f) {
 __device__ __forceinline__ uint64_t abs_bits(double a) {
   return (uint64_t)__double_as_longlong(a) & 0x7FFFFFFFFFFFFFFFull;
 }
-// upper bound of e used for discarded energy: floor(e) + 1, and 0 for an exact zero
-__device__ __forceinline__ uint64_t e_hi(double a, double f) {
-  return e_lo(a, f) + (abs_bits(a) != 0 ? 1ull : 0ull);
+// strict upper bound of e used for discarded energy: floor(e) + 1
+__device__ __forceinline__ uint64_t e_hi(double a, double f) { return e_lo(a, f) + 1ull; }
+// x * 2^e, exact for results in the normal range (cheap common case of ldexp)
+__device__ __forceinline__ double scale2(double x, int e) {
+  return (e >= -1022 && e <= 1023) ? __dmul_rn(x, pow2d(e)) : ldexp(x, e);
 }
 
 // ---------------------------------------------------------------------------

@@ -67,7 +67,7 @@ __device__ __noinline__ void radix_select16(const double* vin, int lane, uint64_
                                             unsigned long long* hist, uint64_t* out) {
   double v[16];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = vin[r];
+  for (int r = 0; r < 16; ++r) v[r] = vin[r * 32 + lane];
   uint64_t klo = ~0ull, khi = 0;
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
@@ -81,7 +81,7 @@ __device__ __noinline__ void radix_select16(const double* vin, int lane, uint64_
   for (;;) {
     const uint64_t span = khi - klo;
     if (span == 0) {
-      const uint64_t h = klo ? e_lo(__longlong_as_double((long long)klo), f) + 1 : 0ull;
+      const uint64_t h = e_lo(__longlong_as_double((long long)klo), f) + 1;
       uint32_t cnt = 0;
 #pragma unroll
       for (int r = 0; r < 16; ++r) cnt += (abs_bits(v[r]) == klo);
@@ -173,7 +173,7 @@ struct Sel16 {
   bool nonfinite;
 };
 
-// v[r] = coefficient 16*lane + r of the warp's block.  scratch: 16 doubles per lane.
+// v[r] = coefficient 16*lane + r of the warp's block.  scratch: shared [16][32] doubles.
 __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t eps_q, unsigned long long* hist,
                                           double* scratch) {
   Sel16 s{0u, 0ull, 0ull, 0, false};
@@ -204,28 +204,34 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
     k = 1023;
   }
   const double f = pow2d(k);
-  uint64_t lo[16];
+  // t_r = 2^52 + floor(e_r) exactly (round-down add); its bit pattern is C + lo_r
+  constexpr uint64_t C52 = 0x4330000000000000ull;
+  double t[16];
   uint64_t t0 = 0, t1 = 0;
 #pragma unroll
   for (int r = 0; r < 16; r += 2) {
-    lo[r] = e_lo(v[r], f);
-    lo[r + 1] = e_lo(v[r + 1], f);
-    t0 += lo[r];
-    t1 += lo[r + 1];
+    const double xa = __dmul_rn(v[r], f), xb = __dmul_rn(v[r + 1], f);
+    t[r] = __dadd_rd(__dmul_rn(xa, xa), 4503599627370496.0);
+    t[r + 1] = __dadd_rd(__dmul_rn(xb, xb), 4503599627370496.0);
+    t0 += (uint64_t)__double_as_longlong(t[r]);
+    t1 += (uint64_t)__double_as_longlong(t[r + 1]);
   }
-  const uint64_t T = warp_sum_u58(t0 + t1);
+  const uint64_t T = warp_sum_u58(t0 + t1 - 16 * C52);
   s.T = T;
   const uint64_t thr = __umul64hi(T, eps_q);
+  // kept-above-threshold set H: hi = lo + 1 > thr  <=>  lo >= thr  <=>  t >= 2^52 + thr
+  const double tthr = 4503599627370496.0 + (double)(thr < (1ull << 51) ? thr : (1ull << 51));
   uint32_t mH = 0;
-  uint64_t n0 = 0, n1 = 0;
+  uint64_t h0 = 0, h1s = 0;
 #pragma unroll
   for (int r = 0; r < 16; r += 2) {
-    const uint64_t ha = lo[r] + (abs_bits(v[r]) != 0 ? 1ull : 0ull);
-    const uint64_t hb = lo[r + 1] + (abs_bits(v[r + 1]) != 0 ? 1ull : 0ull);
-    if (ha > thr) mH |= 1u << r; else n0 += ha;
-    if (hb > thr) mH |= 1u << (r + 1); else n1 += hb;
+    if (t[r] >= tthr) { mH |= 1u << r; h0 += (uint64_t)__double_as_longlong(t[r]); }
+    if (t[r + 1] >= tthr) { mH |= 1u << (r + 1); h1s += (uint64_t)__double_as_longlong(t[r + 1]); }
   }
-  const uint64_t SN = warp_sum_u58(n0 + n1);
+  const uint32_t nH = (uint32_t)__popc(mH);
+  const uint64_t SH = warp_sum_u58(h0 + h1s - nH * C52);  // sum of lo over H
+  const uint32_t NH = __reduce_add_sync(0xffffffffu, nH);
+  const uint64_t SN = T - SH + (512u - NH);                  // sum of hi over the rest
   if (SN <= thr) {
     s.mask = mH;
     s.hdisc = SN;
@@ -242,13 +248,14 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
     const uint64_t gmk = warp_max_u64(mk);
     const uint32_t cand = (mk == gmk && mi < 16) ? (uint32_t)(16 * lane + mi) : 0xffffu;
     const uint32_t gidx = __reduce_min_sync(0xffffffffu, cand);
-    const uint64_t h1 = gmk ? e_lo(__longlong_as_double((long long)gmk), f) + 1ull : 0ull;
-    if (gmk != 0 && SN - h1 <= thr) {
+    const uint64_t h1 = e_lo(__longlong_as_double((long long)gmk), f) + 1ull;
+    if (gidx != 0xffffu && SN - h1 <= thr) {
       s.mask = mH | (((int)(gidx >> 4) == lane) ? (1u << (gidx & 15)) : 0u);
       s.hdisc = SN - h1;
     } else {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) scratch[r] = v[r];
+      for (int r = 0; r < 16; ++r) scratch[r * 32 + lane] = v[r];
+      __syncwarp();
       uint64_t res[3];
       radix_select16(scratch, lane, thr, f, hist, res);
       const uint64_t tstar = res[0];
@@ -303,7 +310,6 @@ __global__ void __launch_bounds__(kF8Warps * 32) compress8_kernel(CompressArgs A
 #pragma unroll
   for (int s = 0; s < kF8Stages; ++s) issue(gw + s * W, s);
   double tot_acc = 0.0, disc_acc = 0.0;
-  double scratch[16];
   int st = 0;
   uint32_t ph = 0;
   for (uint64_t blk = gw; blk < B; blk += W) {
@@ -341,12 +347,10 @@ __global__ void __launch_bounds__(kF8Warps * 32) compress8_kernel(CompressArgs A
         v[kyi * 8 + 2 * q] = t.x;
         v[kyi * 8 + 2 * q + 1] = t.y;
       }
-    fence_proxy_async();
     __syncwarp();
-    issue(blk + kF8Stages * W, st);  // refill this stage
-    st = (st + 1 == kF8Stages) ? 0 : st + 1;
     lines<8, 1, 0, 8, 2, false>(v);  // x sweep: v[r] = coefficient 16*lane + r
-    const Sel16 sel = select16(v, lane, A.eps_q, hist, scratch);
+    double* coef = reinterpret_cast<double*>(sb);  // stage reused as [16][32] scratch
+    const Sel16 sel = select16(v, lane, A.eps_q, hist, coef);
     if (sel.nonfinite && lane == 0) atomicOr(A.ws.flags, kFlagNonFinite);
     const uint32_t mask = sel.nonfinite ? 0u : sel.mask;
     const uint32_t nk = (uint32_t)__popc(mask);
@@ -358,13 +362,28 @@ __global__ void __launch_bounds__(kF8Warps * 32) compress8_kernel(CompressArgs A
         for (uint64_t pb = B; pb < ((B + 3) & ~3ull); ++pb) counts[pb] = 0;  // pad to 16 B
     }
     masks16[blk * 32 + lane] = (uint16_t)mask;
-    double* dst = A.vslot + blk * 512 + off;
+    // kept values: lanes holding any park their 16 coefficients in the stage, then
+    // walk their set bits (few per lane for smooth fields)
+    if (mask) {
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
-      if ((mask >> r) & 1u) *dst++ = v[r];
+      for (int r = 0; r < 16; ++r) coef[r * 32 + lane] = v[r];
+    }
+    {
+      double* dst = A.vslot + blk * 512 + off;
+      uint32_t m = mask;
+      while (m) {
+        const int r = __ffs(m) - 1;
+        m &= m - 1;
+        *dst++ = coef[r * 32 + lane];
+      }
+    }
+    fence_proxy_async();
+    __syncwarp();
+    issue(blk + kF8Stages * W, st);  // refill this stage
+    st = (st + 1 == kF8Stages) ? 0 : st + 1;
     if (!sel.nonfinite && sel.T) {
-      tot_acc += ldexp((double)sel.T, -2 * sel.k);
-      disc_acc += ldexp((double)sel.hdisc, -2 * sel.k);
+      tot_acc += scale2((double)sel.T, -2 * sel.k);
+      disc_acc += scale2((double)sel.hdisc, -2 * sel.k);
     }
   }
   if (lane == 0) {

@@ -15,6 +15,12 @@
 #include "../../include/isf_lossy.h"
 #include "dlt_fast8.cuh"
 
+namespace isf {
+namespace host {
+void build_operators(int lx, double* F, double* B, double* xd, double* wd);
+}
+}  // namespace isf
+
 using namespace isf::dev;
 
 namespace {
@@ -38,68 +44,7 @@ int fail(int code, const char* fmt, ...) {
       return fail(ISF_E_TASK_FAILED, "%s failed: %s", #expr, cudaGetErrorString(_e));     \
   } while (0)
 
-// ---------------------------------------------------------------------------
-// GLL operators in long double (same recipe as DESIGN.md 3.1-3.2): nodes are
-// +-1 and the roots of P'_N by Newton, mirrored exactly; weights 2/(N(N+1)P_N^2);
-// F[k][i] = w_i L_k(x_i)/sqrt(g_k), B[i][k] = L_k(x_i)/sqrt(g_k), g_k = 2/(2k+1),
-// g_N = 2/N; parity (-1)^k enforced bitwise by mirroring.
-// ---------------------------------------------------------------------------
-void legendre_ld(int N, long double x, long double* P) {
-  P[0] = 1.0L;
-  if (N >= 1) P[1] = x;
-  for (int k = 2; k <= N; ++k)
-    P[k] = ((long double)(2 * k - 1) * x * P[k - 1] - (long double)(k - 1) * P[k - 2]) / (long double)k;
-}
-
-void gll_nodes_ld(int lx, long double* x, long double* w) {
-  const int N = lx - 1;
-  long double P[kMaxLx + 1];
-  for (int i = 0; i <= N; ++i) {
-    long double xi = -cosl(3.14159265358979323846264338327950288L * (long double)i / (long double)N);
-    for (int it = 0; it < 100; ++it) {
-      legendre_ld(N, xi, P);
-      const long double dx = (xi * P[N] - P[N - 1]) / ((long double)(N + 1) * P[N]);
-      xi -= dx;
-      if (fabsl(dx) < 1e-30L) break;
-    }
-    x[i] = xi;
-  }
-  x[0] = -1.0L;
-  x[N] = 1.0L;
-  for (int i = 0; i < lx / 2; ++i) x[N - i] = -x[i];
-  if (lx % 2) x[lx / 2] = 0.0L;
-  for (int i = 0; i <= N; ++i) {
-    legendre_ld(N, x[i], P);
-    w[i] = 2.0L / ((long double)N * (long double)(N + 1) * P[N] * P[N]);
-  }
-  for (int i = 0; i < lx / 2; ++i) w[N - i] = w[i];
-}
-
-void build_operators(int lx, double* F, double* B, double* xd, double* wd) {
-  const int N = lx - 1;
-  long double x[kMaxLx], w[kMaxLx], P[kMaxLx + 1];
-  gll_nodes_ld(lx, x, w);
-  for (int i = 0; i < lx; ++i) {
-    if (xd) xd[i] = (double)x[i];
-    if (wd) wd[i] = (double)w[i];
-  }
-  for (int i = 0; i < (lx + 1) / 2; ++i) {
-    legendre_ld(N, x[i], P);
-    for (int k = 0; k < lx; ++k) {
-      const long double g = (k < N) ? 2.0L / (long double)(2 * k + 1) : 2.0L / (long double)N;
-      const long double rs = 1.0L / sqrtl(g);
-      double f = (double)(w[i] * P[k] * rs);
-      double b = (double)(P[k] * rs);
-      if ((lx % 2) && i == lx / 2 && (k % 2)) { f = 0.0; b = 0.0; }
-      F[k * lx + i] = f;
-      B[i * lx + k] = b;
-      if (i != N - i) {
-        F[k * lx + (N - i)] = (k % 2) ? -f : f;
-        B[(N - i) * lx + k] = (k % 2) ? -b : b;
-      }
-    }
-  }
-}
+using isf::host::build_operators;  // gll_host.cpp (binary128 host code)
 
 std::mutex g_init_mu;
 bool g_dev_init[64] = {};
