@@ -1,0 +1,184 @@
+#pragma once
+
+// isf/tasks/lossy.hpp -- the in-situ lossy-compression task of the reference
+// framework, the header that proj/include/isf/core/frame.hpp:11 refers to
+// ("payload_kind 1 carries a compressed block (see tasks/lossy.hpp)") but that
+// the reference never shipped.  Header-only C++ host API with the SPEC.md
+// signatures and the reference's conventions (owned values, isf::Error with an
+// isf::ErrorCode, proj/include/isf/core/errors.hpp:43-52), implemented by the
+// B200 kernels behind the C ABI of include/isf_lossy.h (libisf_lossy.so).
+//
+//   SPEC.md:204-207  LossyConfig          SPEC.md:212-215  CompressionReport (Eq. 1)
+//   SPEC.md:208-211  CompressedBlock      SPEC.md:222-230  lossy_compress
+//   SPEC.md:231-239  lossy_decompress     SPEC.md:282      kind-1 frame payload
+//
+// Drop-in: put this file at proj/include/isf/tasks/lossy.hpp, add include/ to the
+// include path and link libisf_lossy.so.  The transform is the
+// per-element Legendre/GLL DLT of north_star (SPEC.md:205 says DCT-II).
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "isf/core/errors.hpp"
+#include "isf/core/frame.hpp"
+#include "isf/core/types.hpp"
+#include "isf_lossy.h"
+
+namespace isf::tasks {
+
+enum class ErrorNorm { RelativeL2 = ISF_NORM_RELATIVE_L2, RelativeLInf = ISF_NORM_RELATIVE_LINF };
+
+struct LossyConfig {
+    double max_error = 1e-2;  // SPEC.md:205 paper value
+    ErrorNorm error_norm = ErrorNorm::RelativeL2;
+
+    void validate() const {
+        if (!(max_error > 0.0 && max_error < 1.0))
+            throw Error(ErrorCode::InvalidArgument, "LossyConfig: max_error must be in (0,1)");
+        if (error_norm != ErrorNorm::RelativeL2)
+            throw Error(ErrorCode::InvalidArgument, "LossyConfig: only RelativeL2 truncation is implemented");
+    }
+};
+
+struct CompressionReport {
+    std::uint64_t original_size = 0;
+    std::uint64_t compressed_size = 0;
+    double cr = 0.0;  // == (original - compressed) / original in fp64 (Eq. 1)
+
+    static CompressionReport from_sizes(std::uint64_t orig, std::uint64_t comp) {
+        return {orig, comp, isf_lossy_compression_ratio(orig, comp)};
+    }
+};
+
+struct ErrorReport {
+    double err2 = 0, nrm2 = 0, err_inf = 0, u_inf = 0;
+    double rel_l2() const { return nrm2 == 0.0 ? (err2 == 0.0 ? 0.0 : 1.0 / 0.0) : __builtin_sqrt(err2 / nrm2); }
+    double rel_linf() const { return u_inf == 0.0 ? (err_inf == 0.0 ? 0.0 : 1.0 / 0.0) : err_inf / u_inf; }
+};
+
+/// SPEC.md:208-211.  `stream` is the device encoding of include/isf_lossy.h
+/// (counts | masks | values) copied to the host; codec 0 / empty coded bytes
+/// until a lossless stage runs on it.
+struct CompressedBlock {
+    std::uint32_t elements_per_axis = 0;
+    std::uint32_t points_per_element_axis = 0;
+    std::uint32_t components = 0;
+    std::uint64_t n_elements = 0;
+    std::uint64_t kept_total = 0;
+    Bytes stream;
+    std::uint16_t lossless_codec = 0;
+    Bytes coded_bytes;
+    CompressionReport report;
+
+    /// kind-1 payload (SPEC.md:282 codec trailer appended to the stream)
+    Bytes payload() const {
+        Bytes out(stream);
+        put_u16(out, lossless_codec);
+        put_u64(out, coded_bytes.size());
+        out.insert(out.end(), coded_bytes.begin(), coded_bytes.end());
+        return out;
+    }
+    /// core frame with payload_kind = 1, ready for StageWriter::write_frame
+    Bytes frame(std::uint64_t step_index = 0, double sim_time = 0.0) const {
+        FrameHeader h;
+        h.kind = PayloadKind::CompressedBlock;
+        h.step_index = step_index;
+        h.sim_time = sim_time;
+        h.elements_per_axis = elements_per_axis;
+        h.points_per_element_axis = points_per_element_axis;
+        h.components = components;
+        auto p = payload();
+        h.payload_len = p.size();
+        return build_frame(h, p);
+    }
+};
+
+namespace detail {
+inline void check(int rc) {
+    if (rc != 0) throw Error(static_cast<ErrorCode>(rc - 1), isf_lossy_last_error());
+}
+/// One plan per (device, P, components), created on first use on this thread.
+class Plan {
+  public:
+    Plan(std::uint32_t P, std::uint32_t comps, int device) { check(isf_lossy_plan_create(&p_, P, comps, device)); }
+    ~Plan() { isf_lossy_plan_destroy(p_); }
+    Plan(const Plan&) = delete;
+    Plan& operator=(const Plan&) = delete;
+    isf_lossy_plan* get() const { return p_; }
+
+  private:
+    isf_lossy_plan* p_ = nullptr;
+};
+inline isf_lossy_plan* plan_for(std::uint32_t P, std::uint32_t comps) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    struct Key { std::uint32_t P, c; int d; };
+    thread_local std::vector<std::pair<Key, Plan*>> plans;
+    for (auto& kv : plans)
+        if (kv.first.P == P && kv.first.c == comps && kv.first.d == dev) return kv.second->get();
+    plans.push_back({Key{P, comps, dev}, new Plan(P, comps, dev)});
+    return plans.back().second->get();
+}
+}  // namespace detail
+
+/// compress a host Field (H2D, kernels, D2H inside the call).
+inline CompressedBlock lossy_compress(const Field& f, const LossyConfig& cfg) {
+    f.validate();
+    cfg.validate();
+    auto* plan = detail::plan_for(f.points_per_element_axis, f.components);
+    CompressedBlock b;
+    b.elements_per_axis = f.elements_per_axis;
+    b.points_per_element_axis = f.points_per_element_axis;
+    b.components = f.components;
+    b.n_elements = f.element_count();
+    const std::uint64_t cap = isf_lossy_stream_capacity(f.points_per_element_axis, f.components, b.n_elements);
+    b.stream.resize(cap);
+    std::uint64_t n = 0;
+    isf_lossy_stats st{};
+    detail::check(isf_lossy_compress_host(plan, f.values.data(), b.n_elements, cfg.max_error,
+                                          static_cast<int>(cfg.error_norm), b.stream.data(), cap, &n, &st));
+    b.stream.resize(n);
+    b.kept_total = st.kept;
+    b.report = CompressionReport::from_sizes(st.field_bytes, n);
+    return b;
+}
+
+/// decompress to a host Field of the original shape.
+inline Field lossy_decompress(const CompressedBlock& b, const Field& shape, ErrorReport* report = nullptr,
+                              const Field* original = nullptr) {
+    if (b.points_per_element_axis != shape.points_per_element_axis || b.components != shape.components ||
+        b.n_elements != shape.element_count())
+        throw Error(ErrorCode::ShapeMismatch, "compressed block does not match the requested field shape");
+    auto* plan = detail::plan_for(b.points_per_element_axis, b.components);
+    std::vector<double> out(shape.value_count());
+    isf_lossy_stats st{};
+    detail::check(isf_lossy_decompress_host(plan, b.stream.data(), b.stream.size(), b.n_elements, out.data(),
+                                            original ? original->values.data() : nullptr, &st));
+    if (report) *report = ErrorReport{st.err2, st.nrm2, st.err_inf, st.u_inf};
+    return Field(shape.elements_per_axis, shape.points_per_element_axis, shape.components, std::move(out),
+                 shape.domain_length);
+}
+
+/// Device-resident in-situ use (the field already lives in HBM): asynchronous on
+/// `stream`; the field must not be overwritten until the work completed
+/// (handoff rule, proj/include/isf/staging/staging.hpp:5-9).
+inline void lossy_compress_device(const double* d_field, std::uint64_t n_elements, std::uint32_t P,
+                                  std::uint32_t comps, const LossyConfig& cfg, void* d_stream,
+                                  std::uint64_t capacity, isf_lossy_stats* d_stats, cudaStream_t stream) {
+    cfg.validate();
+    detail::check(isf_lossy_compress_async(detail::plan_for(P, comps), d_field, n_elements, cfg.max_error,
+                                           static_cast<int>(cfg.error_norm), d_stream, capacity, d_stats, stream));
+}
+
+inline void lossy_decompress_device(const void* d_stream, std::uint64_t stream_bytes, std::uint64_t n_elements,
+                                    std::uint32_t P, std::uint32_t comps, double* d_out, const double* d_original,
+                                    isf_lossy_stats* d_stats, cudaStream_t stream) {
+    detail::check(isf_lossy_decompress_async(detail::plan_for(P, comps), d_stream, stream_bytes, n_elements, d_out,
+                                             d_original, d_stats, stream));
+}
+
+}  // namespace isf::tasks

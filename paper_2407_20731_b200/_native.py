@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libisf_lossy.so")
+# ISF_LOSSY_LIB: development knob to load an alternative in-tree build (variant timing)
+LIB_PATH = os.environ.get("ISF_LOSSY_LIB") or os.path.join(_HERE, "libisf_lossy.so")
 
 # every symbol declared in include/isf_lossy.h
 EXPORTS = (

@@ -27,10 +27,10 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, log: str | None = None) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, log: str | None = None, out: str = OUT, defines=()) -> str:
+    if not force and out == OUT and not needs_build():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT, *SRC, "-ldl", "-lquadmath"]
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", out, *SRC, "-ldl", "-lquadmath"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if log:
         with open(log, "w") as f:

@@ -20,7 +20,14 @@
 namespace isf {
 namespace dev {
 
-constexpr int kF8Warps = 16;   // warps per CTA
+#ifndef ISF_C8_WARPS
+#define ISF_C8_WARPS 16
+#endif
+#ifndef ISF_D8_WARPS
+#define ISF_D8_WARPS 16
+#endif
+constexpr int kC8Warps = ISF_C8_WARPS;  // compress warps per CTA
+constexpr int kD8Warps = ISF_D8_WARPS;  // decompress warps per CTA
 constexpr int kF8Stages = 2;   // TMA ring depth per warp
 
 // 16-byte chunk c (0..31) of plane kz (512 B)
@@ -115,17 +122,28 @@ __device__ __noinline__ void radix_select16(const double* vin, int lane, uint64_
     }
     const int bits = 64 - __clzll((long long)span);
     const int shift = bits > 6 ? bits - 6 : 0;
-    hist[lane] = 0ull;
-    hist[lane + 32] = 0ull;
+    // 64 bins of energy sums as three 21-bit digit planes of native 32-bit shared
+    // atomics (each value < 2^51, 512 values: every plane sum stays < 2^31)
+    uint32_t* h32 = reinterpret_cast<uint32_t*>(hist);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) h32[lane + 32 * j] = 0u;
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const uint64_t k = abs_bits(v[r]);
-      if (k >= klo && k <= khi)
-        atomicAdd(&hist[(k - klo) >> shift], (unsigned long long)(e_lo(v[r], f) + 1ull));
+      if (k >= klo && k <= khi) {
+        const uint32_t bin = (uint32_t)((k - klo) >> shift);
+        const uint64_t h = e_lo(v[r], f) + 1ull;
+        atomicAdd(&h32[bin], (uint32_t)(h & 0x1FFFFFu));
+        atomicAdd(&h32[64 + bin], (uint32_t)((h >> 21) & 0x1FFFFFu));
+        atomicAdd(&h32[128 + bin], (uint32_t)(h >> 42));
+      }
     }
     __syncwarp();
-    const uint64_t b0 = hist[2 * lane], b1 = hist[2 * lane + 1];
+    const uint64_t b0 = (uint64_t)h32[2 * lane] + ((uint64_t)h32[64 + 2 * lane] << 21) +
+                        ((uint64_t)h32[128 + 2 * lane] << 42);
+    const uint64_t b1 = (uint64_t)h32[2 * lane + 1] + ((uint64_t)h32[64 + 2 * lane + 1] << 21) +
+                        ((uint64_t)h32[128 + 2 * lane + 1] << 42);
     __syncwarp();
     const uint64_t run = b0 + b1;
     uint64_t x = run;
@@ -238,15 +256,16 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   } else {
     // One-move path: the last element of the non-kept prefix (largest |a|, smallest
     // index among ties) joins the kept set if that suffices.
-    uint64_t mk = 0;
-    int mi = 16;
+    double md = -1.0;
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const uint64_t kk = ((mH >> r) & 1u) ? 0ull : abs_bits(v[r]);
-      if (kk > mk) { mk = kk; mi = r; }
+    for (int r = 0; r < 16; ++r) md = fmax(md, ((mH >> r) & 1u) ? -1.0 : fabs(v[r]));
+    const uint64_t gmk = warp_max_u64(md < 0.0 ? 0ull : abs_bits(md));
+    uint32_t cand = 0xffffu;
+    if (md >= 0.0 && abs_bits(md) == gmk) {
+#pragma unroll
+      for (int r = 15; r >= 0; --r)
+        if (!((mH >> r) & 1u) && abs_bits(v[r]) == gmk) cand = (uint32_t)(16 * lane + r);
     }
-    const uint64_t gmk = warp_max_u64(mk);
-    const uint32_t cand = (mk == gmk && mi < 16) ? (uint32_t)(16 * lane + mi) : 0xffffu;
     const uint32_t gidx = __reduce_min_sync(0xffffffffu, cand);
     const uint64_t h1 = e_lo(__longlong_as_double((long long)gmk), f) + 1ull;
     if (gidx != 0xffffu && SN - h1 <= thr) {
@@ -260,6 +279,9 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
       radix_select16(scratch, lane, thr, f, hist, res);
       const uint64_t tstar = res[0];
       const uint32_t icut = (uint32_t)res[1];
+      // reload instead of keeping 32 registers live across the call
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = scratch[r * 32 + lane];
       uint32_t mk2 = 0;
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
@@ -280,20 +302,20 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
 }
 
 // --------------------------- compress ---------------------------------------
-constexpr int kC8WarpBytes = kF8Stages * 4096 + 512 + 128;  // stages | hist | mbarriers
-constexpr int kC8Smem = kF8Warps * kC8WarpBytes;
+constexpr int kC8WarpBytes = kF8Stages * 4096 + 768 + 128;  // stages | hist (3 x 64 u32) | mbarriers
+constexpr int kC8Smem = kC8Warps * kC8WarpBytes;
 
-__global__ void __launch_bounds__(kF8Warps * 32) compress8_kernel(CompressArgs A) {
+__global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned char* wbase = smem + warp * kC8WarpBytes;
   unsigned long long* hist = reinterpret_cast<unsigned long long*>(wbase + kF8Stages * 4096);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kF8Stages * 4096 + 512);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kF8Stages * 4096 + 768);
   const int kzp = lane >> 2, qp = lane & 3;  // y-line / x-line roles
   uint32_t* counts = reinterpret_cast<uint32_t*>(A.stream);
   uint16_t* masks16 = reinterpret_cast<uint16_t*>(A.stream + A.mask_off);
-  const uint64_t W = (uint64_t)gridDim.x * kF8Warps;
-  const uint64_t gw = (uint64_t)blockIdx.x * kF8Warps + warp;
+  const uint64_t W = (uint64_t)gridDim.x * kC8Warps;
+  const uint64_t gw = (uint64_t)blockIdx.x * kC8Warps + warp;
   const uint64_t B = A.nblocks;
   if (lane == 0) {
 #pragma unroll
@@ -356,25 +378,29 @@ __global__ void __launch_bounds__(kF8Warps * 32) compress8_kernel(CompressArgs A
     const uint32_t nk = (uint32_t)__popc(mask);
     const uint32_t off = warp_exscan_u32(nk, lane);
     const uint32_t kept = __shfl_sync(0xffffffffu, off + nk, 31);
-    if (lane == 0) {
-      counts[blk] = kept;
-      if (blk + 1 == B)
-        for (uint64_t pb = B; pb < ((B + 3) & ~3ull); ++pb) counts[pb] = 0;  // pad to 16 B
-    }
+    if (lane == 0) counts[blk] = kept;  // the 16-B pad is zeroed by block_offsets8_kernel
     masks16[blk * 32 + lane] = (uint16_t)mask;
-    // kept values: lanes holding any park their 16 coefficients in the stage, then
-    // walk their set bits (few per lane for smooth fields)
+    // kept values: lanes holding any park their coefficients in the stage as
+    // [pair][lane] double2, then output slot j is written by lane j % 32 (coalesced)
+    double2* coef2 = reinterpret_cast<double2*>(sb);
     if (mask) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) coef[r * 32 + lane] = v[r];
+      for (int r = 0; r < 8; ++r) coef2[r * 32 + lane] = make_double2(v[2 * r], v[2 * r + 1]);
     }
-    {
-      double* dst = A.vslot + blk * 512 + off;
-      uint32_t m = mask;
-      while (m) {
-        const int r = __ffs(m) - 1;
-        m &= m - 1;
-        *dst++ = coef[r * 32 + lane];
+    __syncwarp();
+    for (uint32_t j0 = 0; j0 < kept; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      int own = 0;  // last lane whose first output slot is <= j
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint32_t oc = __shfl_sync(0xffffffffu, off, own + step);
+        if (oc <= j) own += step;
+      }
+      const uint32_t mo = __shfl_sync(0xffffffffu, mask, own);
+      const uint32_t oo = __shfl_sync(0xffffffffu, off, own);
+      if (j < kept) {
+        const uint32_t r = __fns(mo, 0, (int)(j - oo + 1));
+        A.vslot[blk * 512 + j] = reinterpret_cast<const double*>(coef2)[((r >> 1) * 32 + own) * 2 + (r & 1)];
       }
     }
     fence_proxy_async();
@@ -446,7 +472,11 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
     if (b < nblocks) off[b] = excl;
     if (b + 1 == nblocks) {
       off[nblocks] = excl + v;
-      if (vslot && excl + v > cap_vals) atomicOr(ws.flags, kFlagOverflow);
+      if (vslot) {
+        if (excl + v > cap_vals) atomicOr(ws.flags, kFlagOverflow);
+        uint32_t* wcounts = const_cast<uint32_t*>(counts);  // compress: the output stream
+        for (uint64_t pb = nblocks; pb < ((nblocks + 3) & ~3ull); ++pb) wcounts[pb] = 0;  // pad to 16 B
+      }
     }
     __syncthreads();
     if (vslot) {
@@ -467,15 +497,15 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
 // stage: [0,16) the 16-B aligned counts quad | [16,80) mask | [96, ...) values
 constexpr int kD8Stage = 96 + 4096 + 32;
 constexpr int kD8StageBytes = (kD8Stage + 127) & ~127;
-constexpr int kD8WarpBytes = kF8Stages * kD8StageBytes + 128;
-constexpr int kD8Smem = kF8Warps * kD8WarpBytes;
+constexpr int kD8WarpBytes = kF8Stages * kD8StageBytes + 128;  // stages | mbarriers
+constexpr int kD8Smem = kD8Warps * kD8WarpBytes;
 
 struct Decompress8Args {
   DecompressArgs d;
   const uint64_t* off;  // block value offsets (block_offsets8_kernel), off[B] = total
 };
 
-__global__ void __launch_bounds__(kF8Warps * 32) decompress8_kernel(Decompress8Args P) {
+__global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8Args P) {
   const DecompressArgs& A = P.d;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -483,8 +513,8 @@ __global__ void __launch_bounds__(kF8Warps * 32) decompress8_kernel(Decompress8A
   uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kF8Stages * kD8StageBytes);
   const int kzp = lane >> 2, qp = lane & 3;
   const int q = lane & 3, y = lane >> 2;
-  const uint64_t W = (uint64_t)gridDim.x * kF8Warps;
-  const uint64_t gw = (uint64_t)blockIdx.x * kF8Warps + warp;
+  const uint64_t W = (uint64_t)gridDim.x * kD8Warps;
+  const uint64_t gw = (uint64_t)blockIdx.x * kD8Warps + warp;
   const uint64_t B = A.nblocks;
   const uint64_t sb_floor16 = A.stream_bytes & ~15ull;
   const double wxy0 = __dmul_rn(Wg<8>(2 * q), Wg<8>(y));

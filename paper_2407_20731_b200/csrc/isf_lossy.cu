@@ -282,9 +282,9 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
     CUDA_TRY(cudaFuncSetAttribute(compress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
     CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kD8Smem));
     int occ = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel, kF8Warps * 32, kC8Smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel, kC8Warps * 32, kC8Smem));
     p->grid8c = p->sms * std::max(occ, 1);
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel, kF8Warps * 32, kD8Smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel, kD8Warps * 32, kD8Smem));
     p->grid8d = p->sms * std::max(occ, 1);
   }
   CUDA_TRY(ensure(p, 1 << 16, 1 << 14, 1 << 16) == 0 ? cudaSuccess : cudaErrorMemoryAllocation);
@@ -345,7 +345,7 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   if (B >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
   const uint32_t ntiles = (uint32_t)B;  // generic: one tile per block; fast: one warp per block
   const uint32_t nchunks = (ntiles + kOffThreads - 1) / kOffThreads;
-  const size_t nparts = fast ? (size_t)p->grid8c * kF8Warps : (size_t)ntiles;
+  const size_t nparts = fast ? (size_t)p->grid8c * kC8Warps : (size_t)ntiles;
   if (int rc = ensure(p, fast ? nchunks : ntiles, nparts, fast ? B + 1 : 0)) return rc;
   CompressArgs a;
   a.field = d_field;
@@ -371,11 +371,11 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
       p->vslot_cap = slot_bytes;
     }
     a.vslot = p->vslot;
-    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8c, (B + kF8Warps - 1) / kF8Warps);
-    a.ws.total_warps = grid * kF8Warps;
-    compress8_kernel<<<grid, kF8Warps * 32, kC8Smem, s>>>(a);
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8c, (B + kC8Warps - 1) / kC8Warps);
+    a.ws.total_warps = grid * kC8Warps;
+    compress8_kernel<<<grid, kC8Warps * 32, kC8Smem, s>>>(a);
     CUDA_TRY(cudaGetLastError());
-    parts = (uint64_t)grid * kF8Warps;
+    parts = (uint64_t)grid * kC8Warps;
     Workspace wo = a.ws;
     wo.ntiles = nchunks;
     wo.total_warps = std::min<uint32_t>(nchunks, (uint32_t)p->sms * 4);
@@ -439,7 +439,7 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
   if (B >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
   const uint32_t ntiles = (uint32_t)B;
   const uint32_t nchunks = (ntiles + kOffThreads - 1) / kOffThreads;
-  const size_t nparts = fast ? (size_t)p->grid8d * kF8Warps : (size_t)p->sms * 16;
+  const size_t nparts = fast ? (size_t)p->grid8d * kD8Warps : (size_t)p->sms * 16;
   if (int rc = ensure(p, fast ? nchunks : ntiles, nparts, fast ? B + 1 : 0)) return rc;
   DecompressArgs a;
   a.stream = (const uint8_t*)d_stream;
@@ -461,12 +461,12 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
     block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>((const uint8_t*)d_stream, B, p->toff, wo,
                                                                  nullptr, nullptr, 0);
     CUDA_TRY(cudaGetLastError());
-    grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8d, (B + kF8Warps - 1) / kF8Warps);
-    a.ws.total_warps = grid * kF8Warps;
+    grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8d, (B + kD8Warps - 1) / kD8Warps);
+    a.ws.total_warps = grid * kD8Warps;
     Decompress8Args a8{a, p->toff};
-    decompress8_kernel<<<grid, kF8Warps * 32, kD8Smem, s>>>(a8);
+    decompress8_kernel<<<grid, kD8Warps * 32, kD8Smem, s>>>(a8);
     CUDA_TRY(cudaGetLastError());
-    parts = grid * kF8Warps;
+    parts = grid * kD8Warps;
     total_ptr = p->toff + B;
     launches = 3;
   } else {
