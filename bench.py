@@ -50,47 +50,52 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 20 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.proc = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the sampler start before the timed region
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is None:
+            return
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        num = lambda x: float(x) if x.replace(".", "", 1).isdigit() else None
+        sm = sorted(v for v in (num(s[0]) for s in self.samples) if v is not None)
+        mx = max((v for v in (num(s[1]) for s in self.samples) if v is not None), default=None)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
-                          and not s[2 + i].startswith("Not")})
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        pw = [v for v in (num(s[6]) for s in self.samples) if v is not None]
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "power_w_max": max(pw) if pw else None}
 
 
 def cpu_reference(n_samples_el: int, steps: int, warmup: int, threads: int):
@@ -145,13 +150,16 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--cpu-sample-elements", type=int, default=8 * 64 * 64)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--eps", type=float, default=EPS)
+    ap.add_argument("--no-async", action="store_true")
+    ap.add_argument("--async-steps", type=int, default=20)
+    ap.add_argument("--async-every", type=int, default=5)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "native" else args.warmup
     if args.impl == "reference":
@@ -299,12 +307,22 @@ def main():
                      "compress_frac": comp_gbs / hbm, "decompress_frac": deco_gbs / hbm,
                      "step_frac": step_alg_bytes / (ms_per_step * 1e-3) / 1e9 / hbm,
                      "compress_ms_per_field": comp_launch_ms, "decompress_ms_per_field": deco_launch_ms},
-        "quality": {"kept_fraction": [k / nvals for k in kept], "C_over_F": [s / fbytes_field for s in sizes],
+        "quality": {"fields": list(FIELDS), "kept_fraction": [k / nvals for k in kept],
+                    "C_over_F": [s / fbytes_field for s in sizes],
                     "cr": [PK.CompressionReport.from_sizes(fbytes_field, s).cr for s in sizes],
-                    "rel_l2": rel_l2, "rel_linf": rel_linf, "near_threshold_blocks": 0},
+                    "rel_l2": rel_l2, "rel_linf": rel_linf},
         "gpu_launches": 4 * 4 * args.steps,
         "clocks": clk.summary(),
     }
+
+    # cfg5: async in-situ mode -- compression on a low-priority side stream next to a
+    # memory-bound solver stand-in (double-buffered state of the four fields)
+    if not args.no_async:
+        from paper_2407_20731_b200.insitu import AsyncInSitu
+        ai = AsyncInSitu(plan, fields, n_el, eps)
+        result["async_insitu"] = ai.measure(steps=args.async_steps, every=args.async_every)
+        del ai
+        torch.cuda.empty_cache()
 
     # e2e through the host-buffer C ABI (rank-local; H2D + kernels + D2H per call)
     if not args.no_e2e:

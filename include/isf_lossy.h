@@ -158,6 +158,11 @@ int isf_lossy_generate_spectral(isf_lossy_plan* plan, double* d_out, uint64_t bl
                                 uint64_t nblocks, uint64_t seed, const double* h_amp,
                                 void* cuda_stream);
 
+/* Async in-situ mode (cfg5): a memory-bound solver stand-in step
+ * dst = src + alpha*(aux - src) on `cuda_stream` (reads 2n, writes n doubles). */
+int isf_lossy_solver_standin(double* d_dst, const double* d_src, const double* d_aux, uint64_t n,
+                             double alpha, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

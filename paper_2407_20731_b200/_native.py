@@ -21,6 +21,7 @@ EXPORTS = (
     "isf_lossy_decompress_host", "isf_lossy_allreduce", "isf_lossy_compression_ratio",
     "isf_lossy_last_error", "isf_lossy_error_code_name", "isf_lossy_plan_operators",
     "isf_lossy_plan_last_launches", "isf_lossy_generate_tgv", "isf_lossy_generate_spectral",
+    "isf_lossy_solver_standin",
 )
 
 
@@ -71,6 +72,7 @@ def lib() -> ctypes.CDLL:
         "isf_lossy_plan_last_launches": ([P], i32),
         "isf_lossy_generate_tgv": ([P, P, u32, u32, u32, i32, f64, P], i32),
         "isf_lossy_generate_spectral": ([P, P, u64, u64, u64, P, P], i32),
+        "isf_lossy_solver_standin": ([P, P, P, u64, f64, P], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -704,3 +704,33 @@ int isf_lossy_generate_spectral(isf_lossy_plan* p, double* d_out, uint64_t block
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Solver stand-in for the async in-situ mode (cfg5): one explicit relaxation
+// step dst = src + alpha * (aux - src) over n doubles (reads 2n, writes n doubles,
+// the memory-bound profile of an SEM time step).  Not part of the compression path.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void solver_standin_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                      const double* __restrict__ aux, uint64_t n2, double alpha) {
+  const double2* s = reinterpret_cast<const double2*>(src);
+  const double2* a = reinterpret_cast<const double2*>(aux);
+  double2* d = reinterpret_cast<double2*>(dst);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n2; i += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 x = s[i], y = a[i];
+    d[i] = make_double2(__fma_rn(alpha, y.x - x.x, x.x), __fma_rn(alpha, y.y - x.y, x.y));
+  }
+}
+}  // namespace
+
+extern "C" int isf_lossy_solver_standin(double* d_dst, const double* d_src, const double* d_aux, uint64_t n,
+                                        double alpha, void* cuda_stream) {
+  if (!d_dst || !d_src || !d_aux || (n & 1) || (((uintptr_t)d_dst | (uintptr_t)d_src | (uintptr_t)d_aux) & 15))
+    return fail(ISF_E_INVALID_ARGUMENT, "solver stand-in needs 16-B aligned buffers and an even length");
+  int dev = 0, sms = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  solver_standin_kernel<<<sms * 8, 512, 0, (cudaStream_t)cuda_stream>>>(d_dst, d_src, d_aux, n / 2, alpha);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
