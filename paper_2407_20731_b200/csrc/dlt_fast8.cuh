@@ -70,11 +70,11 @@ __device__ __forceinline__ uint32_t warp_exscan_u32(uint32_t v, int lane) {
 // (same algorithm as radix_select in dlt_common.cuh, elements in registers).
 // out = {t*, icut, discarded hi-sum}.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void radix_select16(const double* vin, int lane, uint64_t R, double f,
+__device__ __noinline__ void radix_select16(const double* vin, int lane, uint64_t R, double f, double pre,
                                             unsigned long long* hist, uint64_t* out) {
-  double v[16];
+  double v[16];  // vin: [pair][lane] double2 layout; pre: exact tiny-block pre-scale (else 1)
 #pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = vin[r * 32 + lane];
+  for (int r = 0; r < 16; ++r) v[r] = __dmul_rn(vin[((r >> 1) * 32 + lane) * 2 + (r & 1)], pre);
   uint64_t klo = ~0ull, khi = 0;
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
@@ -191,10 +191,16 @@ struct Sel16 {
   bool nonfinite;
 };
 
-// v[r] = coefficient 16*lane + r of the warp's block.  scratch: shared [16][32] doubles.
+// v[r] = coefficient 16*lane + r of the warp's block (consumed: only pass 0/1 read
+// it); coef2 = the same coefficients parked in shared memory as [pair][lane] double2
+// (read by the one-move and general paths and by the encoder).
 __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t eps_q, unsigned long long* hist,
-                                          double* scratch) {
+                                          const double2* coef2) {
   Sel16 s{0u, 0ull, 0ull, 0, false};
+  auto coef = [&](int r) -> double {
+    const double2 t = coef2[(r >> 1) * 32 + lane];
+    return (r & 1) ? t.y : t.x;
+  };
   uint32_t hm = 0;
 #pragma unroll
   for (int r = 0; r < 16; ++r) hm = ::max(hm, (uint32_t)__double2hiint(v[r]) & 0x7fffffffu);
@@ -214,9 +220,9 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   constexpr int K = energy_K(8);
   int k = K - sexp;
   s.k = k;
-  const bool tiny = k > 1023;  // |a| < 2^-998: exact pre-scale by 2^(k-1023)
-  if (tiny) {
-    const double pre = pow2d(k - 1023);
+  // |a| < 2^-998: exact pre-scale by 2^(k-1023) (applied to every read below)
+  const double pre = k > 1023 ? pow2d(k - 1023) : 1.0;
+  if (k > 1023) {
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = __dmul_rn(v[r], pre);
     k = 1023;
@@ -253,51 +259,39 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   if (SN <= thr) {
     s.mask = mH;
     s.hdisc = SN;
-  } else {
-    // One-move path: the last element of the non-kept prefix (largest |a|, smallest
-    // index among ties) joins the kept set if that suffices.
-    double md = -1.0;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) md = fmax(md, ((mH >> r) & 1u) ? -1.0 : fabs(v[r]));
-    const uint64_t gmk = warp_max_u64(md < 0.0 ? 0ull : abs_bits(md));
-    uint32_t cand = 0xffffu;
-    if (md >= 0.0 && abs_bits(md) == gmk) {
-#pragma unroll
-      for (int r = 15; r >= 0; --r)
-        if (!((mH >> r) & 1u) && abs_bits(v[r]) == gmk) cand = (uint32_t)(16 * lane + r);
-    }
-    const uint32_t gidx = __reduce_min_sync(0xffffffffu, cand);
-    const uint64_t h1 = e_lo(__longlong_as_double((long long)gmk), f) + 1ull;
-    if (gidx != 0xffffu && SN - h1 <= thr) {
-      s.mask = mH | (((int)(gidx >> 4) == lane) ? (1u << (gidx & 15)) : 0u);
-      s.hdisc = SN - h1;
-    } else {
-#pragma unroll
-      for (int r = 0; r < 16; ++r) scratch[r * 32 + lane] = v[r];
-      __syncwarp();
-      uint64_t res[3];
-      radix_select16(scratch, lane, thr, f, hist, res);
-      const uint64_t tstar = res[0];
-      const uint32_t icut = (uint32_t)res[1];
-      // reload instead of keeping 32 registers live across the call
-#pragma unroll
-      for (int r = 0; r < 16; ++r) v[r] = scratch[r * 32 + lane];
-      uint32_t mk2 = 0;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const uint64_t kk = abs_bits(v[r]);
-        const uint32_t j = (uint32_t)(16 * lane + r);
-        if (kk > tstar || (kk == tstar && j < icut)) mk2 |= 1u << r;
-      }
-      s.mask = mk2;
-      s.hdisc = res[2];
-    }
+    return s;
   }
-  if (tiny) {
-    const double un = pow2d(1023 - s.k);
+  // One-move path: the last element of the non-kept prefix (largest |a|, smallest
+  // index among ties) joins the kept set if that suffices.
+  uint64_t mk = 0;
+  int mi = 16;
 #pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = __dmul_rn(v[r], un);
+  for (int r = 0; r < 16; ++r) {
+    const uint64_t kk = ((mH >> r) & 1u) ? 0ull : abs_bits(coef(r)) + 1ull;  // +1: zeros count
+    if (kk > mk) { mk = kk; mi = r; }
   }
+  const uint64_t gmk = warp_max_u64(mk);
+  const uint32_t cand = (mk == gmk && mi < 16) ? (uint32_t)(16 * lane + mi) : 0xffffu;
+  const uint32_t gidx = __reduce_min_sync(0xffffffffu, cand);
+  const uint64_t h1 = gmk ? e_lo(__dmul_rn(__longlong_as_double((long long)(gmk - 1)), pre), f) + 1ull : 0ull;
+  if (gidx != 0xffffu && SN - h1 <= thr) {
+    s.mask = mH | (((int)(gidx >> 4) == lane) ? (1u << (gidx & 15)) : 0u);
+    s.hdisc = SN - h1;
+    return s;
+  }
+  uint64_t res[3];
+  radix_select16(reinterpret_cast<const double*>(coef2), lane, thr, f, pre, hist, res);
+  const uint64_t tstar = res[0];
+  const uint32_t icut = (uint32_t)res[1];
+  uint32_t mk2 = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const uint64_t kk = abs_bits(__dmul_rn(coef(r), pre));
+    const uint32_t j = (uint32_t)(16 * lane + r);
+    if (kk > tstar || (kk == tstar && j < icut)) mk2 |= 1u << r;
+  }
+  s.mask = mk2;
+  s.hdisc = res[2];
   return s;
 }
 
@@ -371,8 +365,13 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       }
     __syncwarp();
     lines<8, 1, 0, 8, 2, false>(v);  // x sweep: v[r] = coefficient 16*lane + r
-    double* coef = reinterpret_cast<double*>(sb);  // stage reused as [16][32] scratch
-    const Sel16 sel = select16(v, lane, A.eps_q, hist, coef);
+    // park the coefficients in the stage as [pair][lane] double2 (conflict free);
+    // the registers are then free for the selection
+    double2* coef2 = reinterpret_cast<double2*>(sb);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) coef2[r * 32 + lane] = make_double2(v[2 * r], v[2 * r + 1]);
+    __syncwarp();
+    const Sel16 sel = select16(v, lane, A.eps_q, hist, coef2);
     if (sel.nonfinite && lane == 0) atomicOr(A.ws.flags, kFlagNonFinite);
     const uint32_t mask = sel.nonfinite ? 0u : sel.mask;
     const uint32_t nk = (uint32_t)__popc(mask);
@@ -380,14 +379,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     const uint32_t kept = __shfl_sync(0xffffffffu, off + nk, 31);
     if (lane == 0) counts[blk] = kept;  // the 16-B pad is zeroed by block_offsets8_kernel
     masks16[blk * 32 + lane] = (uint16_t)mask;
-    // kept values: lanes holding any park their coefficients in the stage as
-    // [pair][lane] double2, then output slot j is written by lane j % 32 (coalesced)
-    double2* coef2 = reinterpret_cast<double2*>(sb);
-    if (mask) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) coef2[r * 32 + lane] = make_double2(v[2 * r], v[2 * r + 1]);
-    }
-    __syncwarp();
+    // kept values from the parked copy: output slot j is written by lane j % 32
     for (uint32_t j0 = 0; j0 < kept; j0 += 32) {
       const uint32_t j = j0 + lane;
       int own = 0;  // last lane whose first output slot is <= j
@@ -420,22 +412,107 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
 
 // --------------------------- block offsets / compact passes -----------------
 // off[b] = sum of counts of blocks < b (exclusive), off[B] = total.  CTA chunks of
-// 256 blocks chained by a decoupled look-back on ws.status with a dynamic chunk
-// claim (deadlock free).  With vslot != nullptr (compress) every block's kept
-// values are then moved from its fixed slot into the packed value region.
+// 1024 blocks (4 per thread) chained by a decoupled look-back on ws.status with a
+// dynamic chunk claim (deadlock free).  With vslot != nullptr (compress) the kept
+// values of the chunk are then moved from their per-block slots into the packed
+// value region (flattened over the chunk: value i of the chunk by thread i % 256),
+// and the last CTA to finish reduces the statistics (fused finalize).
 constexpr int kOffThreads = 256;
+constexpr int kOffPerThread = 4;
+constexpr int kOffChunk = kOffThreads * kOffPerThread;
+
+// Deterministic reduction of the per-warp partials into isf_lossy_stats by one CTA.
+__device__ void finalize_cta(const FinalizeArgs& A, double* s_red /* 4 * warps */) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double a0 = 0.0, a1 = 0.0;
+  unsigned long long x0 = 0, x1 = 0;
+  for (uint64_t i = tid; i < A.nparts; i += blockDim.x) {
+    a0 = __dadd_rn(a0, A.partials[i * 4 + 0]);
+    a1 = __dadd_rn(a1, A.partials[i * 4 + 1]);
+    if (A.mode == 1) {
+      unsigned long long v = (unsigned long long)__double_as_longlong(A.partials[i * 4 + 2]);
+      x0 = v > x0 ? v : x0;
+      v = (unsigned long long)__double_as_longlong(A.partials[i * 4 + 3]);
+      x1 = v > x1 ? v : x1;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a0 = __dadd_rn(a0, __shfl_xor_sync(0xffffffffu, a0, o));
+    a1 = __dadd_rn(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+    unsigned long long t = __shfl_xor_sync(0xffffffffu, x0, o);
+    x0 = t > x0 ? t : x0;
+    t = __shfl_xor_sync(0xffffffffu, x1, o);
+    x1 = t > x1 ? t : x1;
+  }
+  if (lane == 0) {
+    s_red[warp * 4 + 0] = a0;
+    s_red[warp * 4 + 1] = a1;
+    s_red[warp * 4 + 2] = __longlong_as_double((long long)x0);
+    s_red[warp * 4 + 3] = __longlong_as_double((long long)x1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s0 = 0.0, s1 = 0.0;
+    unsigned long long m0 = 0, m1 = 0;
+    for (int w = 0; w < nw; ++w) {
+      s0 = __dadd_rn(s0, s_red[w * 4]);
+      s1 = __dadd_rn(s1, s_red[w * 4 + 1]);
+      const unsigned long long t0 = (unsigned long long)__double_as_longlong(s_red[w * 4 + 2]);
+      const unsigned long long t1 = (unsigned long long)__double_as_longlong(s_red[w * 4 + 3]);
+      m0 = t0 > m0 ? t0 : m0;
+      m1 = t1 > m1 ? t1 : m1;
+    }
+    double* st = reinterpret_cast<double*>(A.stats);
+    uint64_t* su = reinterpret_cast<uint64_t*>(A.stats);
+    const uint64_t total = *A.total_ptr;
+    for (int i = 0; i < 12; ++i) su[i] = 0;
+    if (A.mode == 0) {
+      st[4] = s1;  // disc2
+      st[5] = s0;  // tot2
+    } else if (A.with_error) {
+      st[0] = s0;
+      st[1] = s1;
+      st[2] = __longlong_as_double((long long)m0);
+      st[3] = __longlong_as_double((long long)m1);
+    }
+    su[6] = total;
+    su[7] = A.nblocks;
+    su[8] = A.val_off + 8 * total;
+    su[9] = A.field_bytes;
+    su[10] = *A.flags;
+    *A.flags = 0;
+  }
+}
+
+// Last-CTA election for the fused finalize; `done` is reset by the winner.
+__device__ __forceinline__ bool last_cta(uint32_t* done) {
+  __shared__ uint32_t s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (s_last) {
+      *done = 0;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  return s_last != 0;
+}
 
 __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8_t* stream, uint64_t nblocks,
                                                                     uint64_t* off, Workspace ws,
                                                                     const double* vslot, double* vals,
-                                                                    uint64_t cap_vals) {
+                                                                    uint64_t cap_vals, FinalizeArgs fin) {
   __shared__ uint64_t wsum[kOffThreads / 32];
   __shared__ uint64_t s_prefix;
   __shared__ uint32_t s_chunk;
-  __shared__ uint64_t s_off[kOffThreads + 1];
+  __shared__ uint64_t s_off[kOffChunk + 1];
+  __shared__ double s_red[4 * (kOffThreads / 32)];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t* counts = reinterpret_cast<const uint32_t*>(stream);
-  const uint32_t nchunks = (uint32_t)((nblocks + kOffThreads - 1) / kOffThreads);
+  const uint32_t nchunks = (uint32_t)((nblocks + kOffChunk - 1) / kOffChunk);
   for (;;) {
     if (tid == 0) {
       const uint32_t c = atomicAdd(ws.counter, 1u);
@@ -445,8 +522,13 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
     __syncthreads();
     const uint32_t chunk = s_chunk;
     if (chunk >= nchunks) break;
-    const uint64_t b = (uint64_t)chunk * kOffThreads + tid;
-    const uint64_t v = b < nblocks ? (uint64_t)counts[b] : 0ull;
+    const uint64_t b0 = (uint64_t)chunk * kOffChunk + (uint64_t)tid * kOffPerThread;
+    uint4 c4 = make_uint4(0, 0, 0, 0);
+    if (b0 < nblocks) c4 = *(reinterpret_cast<const uint4*>(counts) + b0 / 4);  // counts padded to 16 B
+    if (b0 + 1 >= nblocks) c4.y = 0;
+    if (b0 + 2 >= nblocks) c4.z = 0;
+    if (b0 + 3 >= nblocks) c4.w = 0;
+    const uint64_t v = (uint64_t)c4.x + c4.y + c4.z + c4.w;
     uint64_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -466,31 +548,46 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
       if (lane == 0) s_prefix = pre;
     }
     __syncthreads();
-    const uint64_t excl = s_prefix + wex + x - v;
-    s_off[tid] = excl;
-    if (tid == kOffThreads - 1) s_off[kOffThreads] = excl + v;
-    if (b < nblocks) off[b] = excl;
-    if (b + 1 == nblocks) {
-      off[nblocks] = excl + v;
+    const uint64_t e0 = s_prefix + wex + x - v;
+    const uint64_t e1 = e0 + c4.x, e2 = e1 + c4.y, e3 = e2 + c4.z;
+    s_off[tid * 4 + 0] = e0;
+    s_off[tid * 4 + 1] = e1;
+    s_off[tid * 4 + 2] = e2;
+    s_off[tid * 4 + 3] = e3;
+    if (tid == kOffThreads - 1) s_off[kOffChunk] = e0 + v;
+    if (b0 < nblocks) {
+      // off[] is 8-byte aligned only: scalar stores
+      off[b0] = e0;
+      if (b0 + 1 < nblocks) off[b0 + 1] = e1;
+      if (b0 + 2 < nblocks) off[b0 + 2] = e2;
+      if (b0 + 3 < nblocks) off[b0 + 3] = e3;
+    }
+    if (b0 < nblocks && b0 + 4 >= nblocks) {
+      off[nblocks] = e0 + v;
       if (vslot) {
-        if (excl + v > cap_vals) atomicOr(ws.flags, kFlagOverflow);
+        if (e0 + v > cap_vals) atomicOr(ws.flags, kFlagOverflow);
         uint32_t* wcounts = const_cast<uint32_t*>(counts);  // compress: the output stream
         for (uint64_t pb = nblocks; pb < ((nblocks + 3) & ~3ull); ++pb) wcounts[pb] = 0;  // pad to 16 B
       }
     }
     __syncthreads();
     if (vslot) {
-      for (int t = warp; t < kOffThreads; t += kOffThreads / 32) {
-        const uint64_t bb = (uint64_t)chunk * kOffThreads + t;
-        if (bb >= nblocks) break;
-        const uint64_t o0 = s_off[t], n = s_off[t + 1] - o0;
-        if (o0 + n > cap_vals) continue;
-        const double* src = vslot + bb * 512;
-        for (uint64_t i = lane; i < n; i += 32) vals[o0 + i] = src[i];
+      const uint64_t first = s_off[0], nval = s_off[kOffChunk] - first;
+      if (first + nval <= cap_vals) {
+        for (uint64_t i = tid; i < nval; i += kOffThreads) {
+          // block t of the chunk holding value i: last t with s_off[t] - first <= i
+          int t = 0;
+#pragma unroll
+          for (int step = kOffChunk / 2; step; step >>= 1)
+            if (t + step < kOffChunk && s_off[t + step] - first <= i) t += step;
+          const uint64_t bb = (uint64_t)chunk * kOffChunk + t;
+          vals[first + i] = vslot[bb * 512 + (first + i - s_off[t])];
+        }
       }
     }
     __syncthreads();
   }
+  if (fin.stats && last_cta(ws.counter + 1)) finalize_cta(fin, s_red);
 }
 
 // --------------------------- decompress -------------------------------------
@@ -503,6 +600,7 @@ constexpr int kD8Smem = kD8Warps * kD8WarpBytes;
 struct Decompress8Args {
   DecompressArgs d;
   const uint64_t* off;  // block value offsets (block_offsets8_kernel), off[B] = total
+  FinalizeArgs fin;     // fused finalize by the last CTA
 };
 
 __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8Args P) {
@@ -655,6 +753,8 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
       A.ws.partials[gw * 4 + 3] = __longlong_as_double((long long)uinf);
     }
   }
+  __shared__ double s_red[4 * kD8Warps];
+  if (last_cta(A.ws.counter + 1)) finalize_cta(P.fin, s_red);
 }
 
 }  // namespace dev

@@ -344,9 +344,9 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   const bool fast = use_fast8(p);
   if (B >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
   const uint32_t ntiles = (uint32_t)B;  // generic: one tile per block; fast: one warp per block
-  const uint32_t nchunks = (ntiles + kOffThreads - 1) / kOffThreads;
+  const uint32_t nchunks8 = (ntiles + kOffChunk - 1) / kOffChunk;
   const size_t nparts = fast ? (size_t)p->grid8c * kC8Warps : (size_t)ntiles;
-  if (int rc = ensure(p, fast ? nchunks : ntiles, nparts, fast ? B + 1 : 0)) return rc;
+  if (int rc = ensure(p, fast ? nchunks8 : ntiles, nparts, fast ? B + 1 : 0)) return rc;
   CompressArgs a;
   a.field = d_field;
   a.nblocks = B;
@@ -377,17 +377,18 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
     CUDA_TRY(cudaGetLastError());
     parts = (uint64_t)grid * kC8Warps;
     Workspace wo = a.ws;
-    wo.ntiles = nchunks;
-    wo.total_warps = std::min<uint32_t>(nchunks, (uint32_t)p->sms * 4);
+    wo.ntiles = nchunks8;
+    wo.total_warps = std::min<uint32_t>(nchunks8, (uint32_t)p->sms * 4);
+    FinalizeArgs f{0, p->partials, parts, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
+                   B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
     block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>(
         a.stream, B, p->toff, wo, p->vslot, reinterpret_cast<double*>(a.stream + a.val_off),
-        capacity > hdr ? (capacity - hdr) / 8 : 0);
+        capacity > hdr ? (capacity - hdr) / 8 : 0, f);  // compaction + fused finalize
     CUDA_TRY(cudaGetLastError());
-    total_ptr = p->toff + B;
-    launches = 3;
-  } else {
-    if (int rc = dispatch_compress_generic(AllLx{}, (int)p->P, p, a, s)) return rc;
+    p->last_launches = 2;
+    return 0;
   }
+  if (int rc = dispatch_compress_generic(AllLx{}, (int)p->P, p, a, s)) return rc;
   FinalizeArgs f{0, p->partials, parts, p->status, total_ptr, ntiles, p->flags, d_stats, B,
                  B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
   finalize_kernel<<<1, kFinThreads, 0, s>>>(f);
@@ -438,9 +439,9 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
   const bool fast = use_fast8(p);
   if (B >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
   const uint32_t ntiles = (uint32_t)B;
-  const uint32_t nchunks = (ntiles + kOffThreads - 1) / kOffThreads;
+  const uint32_t nchunks8 = (ntiles + kOffChunk - 1) / kOffChunk;
   const size_t nparts = fast ? (size_t)p->grid8d * kD8Warps : (size_t)p->sms * 16;
-  if (int rc = ensure(p, fast ? nchunks : ntiles, nparts, fast ? B + 1 : 0)) return rc;
+  if (int rc = ensure(p, fast ? nchunks8 : ntiles, nparts, fast ? B + 1 : 0)) return rc;
   DecompressArgs a;
   a.stream = (const uint8_t*)d_stream;
   a.stream_bytes = stream_bytes;
@@ -456,19 +457,22 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
   int launches = 2;
   if (fast) {
     Workspace wo = a.ws;
-    wo.ntiles = nchunks;
-    wo.total_warps = std::min<uint32_t>(nchunks, (uint32_t)p->sms * 4);
+    wo.ntiles = nchunks8;
+    wo.total_warps = std::min<uint32_t>(nchunks8, (uint32_t)p->sms * 4);
+    FinalizeArgs none{};
     block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>((const uint8_t*)d_stream, B, p->toff, wo,
-                                                                 nullptr, nullptr, 0);
+                                                                 nullptr, nullptr, 0, none);
     CUDA_TRY(cudaGetLastError());
     grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8d, (B + kD8Warps - 1) / kD8Warps);
     a.ws.total_warps = grid * kD8Warps;
-    Decompress8Args a8{a, p->toff};
-    decompress8_kernel<<<grid, kD8Warps * 32, kD8Smem, s>>>(a8);
-    CUDA_TRY(cudaGetLastError());
     parts = grid * kD8Warps;
-    total_ptr = p->toff + B;
-    launches = 3;
+    FinalizeArgs f{1, p->partials, d_original ? parts : 0u, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
+                   B * (uint64_t)p->P * p->P * p->P * 8, hdr, d_original ? 1 : 0};
+    Decompress8Args a8{a, p->toff, f};
+    decompress8_kernel<<<grid, kD8Warps * 32, kD8Smem, s>>>(a8);  // + fused finalize
+    CUDA_TRY(cudaGetLastError());
+    p->last_launches = 2;
+    return 0;
   } else {
     if (int rc = dispatch_decompress_generic(AllLx{}, (int)p->P, p, a, s, &grid)) return rc;
     parts = grid;

@@ -181,7 +181,7 @@ def test_determinism_and_launches(native, oracle):
     a = PK.lossy_compress(f, PK.LossyConfig(1e-3))
     b = PK.lossy_compress(f, PK.LossyConfig(1e-3))
     assert torch.equal(a.stream, b.stream)
-    assert PK.get_plan(8, 1, 0).last_launches() == 3
+    assert PK.get_plan(8, 1, 0).last_launches() == 2
 
 
 def test_host_entry_points(native, oracle):
@@ -210,3 +210,32 @@ def test_device_generators_match_oracle(native, oracle):
     plan.generate_tgv(t, 16, 0)
     tr = oracle.gen_tgv(16, 8, 0)
     assert np.max(np.abs(t.cpu().numpy() - tr)) <= 4e-15  # libm vs CUDA cos/sin: a few ulp
+
+
+@pytest.mark.parametrize("kind", ["spectral", "tgv"])
+def test_determinism_stress(native, oracle, kind):
+    """Repeated runs must give identical streams and statistics (no races in the TMA
+    ring, the parked coefficients, the compaction or the fused finalize)."""
+    import paper_2407_20731_b200 as PK
+    if kind == "spectral":
+        u = oracle.gen_spectral(8, 20000)
+        n_el = 20000
+    else:
+        u = oracle.gen_tgv(32, 8, 3)
+        n_el = 32 ** 3
+    f = _field(8, 1, n_el, u)
+    ref = None
+    refd = None
+    for it in range(6):
+        blk = PK.lossy_compress(f, PK.LossyConfig(1e-3))
+        back, rep = PK.decompress_with_error(blk, f.shape, f)
+        s = blk.stream.cpu().numpy()
+        d = back.values.cpu().numpy()
+        if ref is None:
+            ref, refd, refrep = s, d, rep
+            rc, os_, st = oracle.compress(u, 8, 1, 1e-3)
+            assert np.array_equal(s, os_)
+        else:
+            assert np.array_equal(s, ref), f"stream differs on run {it}"
+            assert np.array_equal(d, refd), f"reconstruction differs on run {it}"
+            assert (rep.err2, rep.nrm2, rep.err_inf, rep.u_inf) == (refrep.err2, refrep.nrm2, refrep.err_inf, refrep.u_inf)

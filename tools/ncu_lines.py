@@ -21,9 +21,12 @@ def main(rep, kernel, so, blocks, top=40):
         data.append(r)
     ad, ex = hdr.index("Address"), hdr.index("Instructions Executed")
     si = hdr.index("Warp Stall Sampling (All Samples)")
-    subprocess.run(["cuobjdump", "-xelf", "all", so], cwd="/tmp", capture_output=True)
-    cub = [l for l in subprocess.run(["ls", "/tmp"], capture_output=True, text=True).stdout.split() if l.endswith(".cubin")]
-    dis = subprocess.run(["nvdisasm", "-g", "-c", "/tmp/" + cub[0]], capture_output=True, text=True).stdout.split("\n")
+    import os
+    import tempfile
+    tmp = tempfile.mkdtemp()
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
+    cub = [l for l in os.listdir(tmp) if l.endswith(".cubin")]
+    dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub[0])], capture_output=True, text=True).stdout.split("\n")
     start = [i for i, l in enumerate(dis) if l.startswith(".text.") and (str(len(kernel)) + kernel) in l][0]
     fl, offmap = None, {}
     for l in dis[start + 1:]:
