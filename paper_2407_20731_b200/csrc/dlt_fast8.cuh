@@ -55,6 +55,20 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t x) {
   const uint32_t lo = hi == mh ? (uint32_t)x : 0xffffffffu;
   return ((uint64_t)mh << 32) | __reduce_min_sync(0xffffffffu, lo);
 }
+// exclusive prefix of per-lane counts v <= 31 without a dependent shuffle chain:
+// five independent ballots over the bits of v
+__device__ __forceinline__ uint32_t warp_exscan_small(uint32_t v, int lane, uint32_t& total) {
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t pre = 0, tot = 0;
+#pragma unroll
+  for (int b = 0; b < 5; ++b) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, (v >> b) & 1u);
+    pre += (uint32_t)__popc(bal & lt) << b;
+    tot += (uint32_t)__popc(bal) << b;
+  }
+  total = tot;
+  return pre;
+}
 __device__ __forceinline__ uint32_t warp_exscan_u32(uint32_t v, int lane) {
   uint32_t x = v;
 #pragma unroll
@@ -263,17 +277,35 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   }
   // One-move path: the last element of the non-kept prefix (largest |a|, smallest
   // index among ties) joins the kept set if that suffices.
-  uint64_t mk = 0;
-  int mi = 16;
+  // t is monotone in |a|: the largest t among the non-kept gives the candidates (its
+  // lo + 1 is the hi to move); ties in t are resolved by |a|, then the smallest index.
+  uint64_t tm = 0;
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    const uint64_t kk = ((mH >> r) & 1u) ? 0ull : abs_bits(coef(r)) + 1ull;  // +1: zeros count
-    if (kk > mk) { mk = kk; mi = r; }
+    const uint64_t tb = ((mH >> r) & 1u) ? 0ull : (uint64_t)__double_as_longlong(t[r]);
+    tm = tb > tm ? tb : tm;
   }
-  const uint64_t gmk = warp_max_u64(mk);
-  const uint32_t cand = (mk == gmk && mi < 16) ? (uint32_t)(16 * lane + mi) : 0xffffu;
-  const uint32_t gidx = __reduce_min_sync(0xffffffffu, cand);
-  const uint64_t h1 = gmk ? e_lo(__dmul_rn(__longlong_as_double((long long)(gmk - 1)), pre), f) + 1ull : 0ull;
+  const uint64_t gtm = warp_max_u64(tm);
+  uint32_t cm = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+    if (!((mH >> r) & 1u) && (uint64_t)__double_as_longlong(t[r]) == gtm) cm |= 1u << r;
+  const uint32_t ncand = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(cm));
+  uint32_t gidx;
+  if (ncand == 1) {
+    gidx = __reduce_min_sync(0xffffffffu, cm ? (uint32_t)(16 * lane + __ffs(cm) - 1) : 0xffffu);
+  } else {
+    uint64_t mk = 0;
+    int mi = 16;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint64_t kk = ((cm >> r) & 1u) ? abs_bits(coef(r)) + 1ull : 0ull;  // +1: zeros count
+      if (kk > mk) { mk = kk; mi = r; }
+    }
+    const uint64_t gmk = warp_max_u64(mk);
+    gidx = __reduce_min_sync(0xffffffffu, (mk == gmk && mi < 16) ? (uint32_t)(16 * lane + mi) : 0xffffu);
+  }
+  const uint64_t h1 = gtm - C52 + 1ull;
   if (gidx != 0xffffu && SN - h1 <= thr) {
     s.mask = mH | (((int)(gidx >> 4) == lane) ? (1u << (gidx & 15)) : 0u);
     s.hdisc = SN - h1;
@@ -374,25 +406,19 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     const Sel16 sel = select16(v, lane, A.eps_q, hist, coef2);
     if (sel.nonfinite && lane == 0) atomicOr(A.ws.flags, kFlagNonFinite);
     const uint32_t mask = sel.nonfinite ? 0u : sel.mask;
-    const uint32_t nk = (uint32_t)__popc(mask);
-    const uint32_t off = warp_exscan_u32(nk, lane);
-    const uint32_t kept = __shfl_sync(0xffffffffu, off + nk, 31);
+    uint32_t kept;
+    const uint32_t off = warp_exscan_small((uint32_t)__popc(mask), lane, kept);
     if (lane == 0) counts[blk] = kept;  // the 16-B pad is zeroed by block_offsets8_kernel
     masks16[blk * 32 + lane] = (uint16_t)mask;
-    // kept values from the parked copy: output slot j is written by lane j % 32
-    for (uint32_t j0 = 0; j0 < kept; j0 += 32) {
-      const uint32_t j = j0 + lane;
-      int own = 0;  // last lane whose first output slot is <= j
-#pragma unroll
-      for (int step = 16; step; step >>= 1) {
-        const uint32_t oc = __shfl_sync(0xffffffffu, off, own + step);
-        if (oc <= j) own += step;
-      }
-      const uint32_t mo = __shfl_sync(0xffffffffu, mask, own);
-      const uint32_t oo = __shfl_sync(0xffffffffu, off, own);
-      if (j < kept) {
-        const uint32_t r = __fns(mo, 0, (int)(j - oo + 1));
-        A.vslot[blk * 512 + j] = reinterpret_cast<const double*>(coef2)[((r >> 1) * 32 + own) * 2 + (r & 1)];
+    // kept values from the parked copy, written by their owner lane in index order
+    {
+      const double* cf = reinterpret_cast<const double*>(coef2) + 2 * lane;
+      double* dst = A.vslot + blk * 512 + off;
+      uint32_t m = mask;
+      while (m) {
+        const int r = __ffs(m) - 1;
+        m &= m - 1;
+        *dst++ = cf[(r >> 1) * 64 + (r & 1)];
       }
     }
     fence_proxy_async();
