@@ -26,6 +26,7 @@ import math
 import os
 import subprocess
 import sys
+import queue
 import threading
 import time
 
@@ -330,22 +331,45 @@ def main():
         hs = [torch.empty(cap, dtype=torch.uint8).pin_memory().numpy() for _ in range(4)]
         ho = torch.empty(nvals, dtype=torch.float64).pin_memory().numpy()
 
-        def e2e_step():
-            h2d = d2h = 0
-            for i in range(4):
-                nb, st = plan.compress_host(hf[i], n_el, eps, hs[i])
-                plan.decompress_host(hs[i], nb, n_el, ho)
-                h2d += fbytes_field + nb
-                d2h += nb + fbytes_field
-            return h2d, d2h
+        # Two plans driven from two host threads: the compress calls are H2D-bound and the
+        # decompress calls D2H-bound, so running field i+1's compress next to field i's
+        # decompress keeps both PCIe directions busy.  Every call is the blocking
+        # host-buffer C ABI; a ring of 4 host stream buffers hands fields over.
+        plan2 = PK.LossyPlan(LX, 1, local)
+        nbs = [0] * 4
 
-        e2e_step()
+        def e2e_run(nsteps):
+            q: "queue.Queue" = queue.Queue(maxsize=2)
+            err = []
+
+            def producer():
+                try:
+                    for j in range(4 * nsteps):
+                        nbs[j % 4], _ = plan.compress_host(hf[j % 4], n_el, eps, hs[j % 4])
+                        q.put(j)
+                except BaseException as e:  # noqa: BLE001
+                    err.append(e)
+                    q.put(None)
+
+            th = threading.Thread(target=producer)
+            th.start()
+            for _ in range(4 * nsteps):
+                j = q.get()
+                if j is None:
+                    break
+                plan2.decompress_host(hs[j % 4], nbs[j % 4], n_el, ho)
+            th.join()
+            if err:
+                raise err[0]
+            h2d = sum(fbytes_field + n for n in nbs)
+            return h2d, h2d
+
+        e2e_run(1)
         if world > 1:
             dist.barrier()
-        k = max(1, min(args.steps, 3))
+        k = max(1, min(args.steps, 5))
         t0 = time.perf_counter()
-        for _ in range(k):
-            h2d, d2h = e2e_step()
+        h2d, d2h = e2e_run(k)
         dt = (time.perf_counter() - t0) / k
         tt = torch.tensor([dt], dtype=torch.float64, device=dev)
         if world > 1:
@@ -353,7 +377,7 @@ def main():
         dt = float(tt.item())
         result["e2e"] = {"value": world * field_bytes_step / dt / 1e9, "unit": UNIT,
                          "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                         "api": "isf_lossy_compress_host + isf_lossy_decompress_host (pinned host buffers)",
+                         "api": "isf_lossy_compress_host + isf_lossy_decompress_host (pinned host buffers; compress of field i+1 overlaps decompress of field i on a second plan)",
                          "steps": k}
 
     if rank == 0 and not args.no_cpu:

@@ -566,6 +566,18 @@ int isf_lossy_decompress_host(isf_lossy_plan* p, const void* h_stream, uint64_t 
 }
 
 // ---- NCCL (resolved at run time) ----
+namespace {
+__global__ void status_lanes_kernel(uint64_t* st, int fold) {
+  const uint64_t v = *st;
+  uint64_t r = 0;
+  for (int k = 0; k < 4; ++k) {
+    if (fold) r |= (((v >> (16 * k)) & 0xFFFFull) != 0) ? (1ull << k) : 0ull;
+    else r |= ((v >> k) & 1ull) << (16 * k);
+  }
+  *st = r;
+}
+}  // namespace
+
 typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*nccl_group_fn)(void);
 
@@ -591,14 +603,19 @@ int isf_lossy_allreduce(isf_lossy_stats* d_stats, void* comm, void* cuda_stream)
   cudaStream_t s = (cudaStream_t)cuda_stream;
   double* d = reinterpret_cast<double*>(d_stats);
   uint64_t* u = reinterpret_cast<uint64_t*>(d_stats);
+  // status is a bit set and NCCL has no OR: spread bit k into 16-bit lane k, sum,
+  // then fold every non-zero lane back to its bit (exact for < 65536 ranks)
+  status_lanes_kernel<<<1, 1, 0, s>>>(u + 10, 0);
   int r = gs();
   r |= ar(d + 0, d + 0, 2, 8, 0, comm, s);   // err2, nrm2
   r |= ar(d + 2, d + 2, 2, 8, 2, comm, s);   // err_inf, u_inf
   r |= ar(d + 4, d + 4, 2, 8, 0, comm, s);   // disc2, tot2
   r |= ar(u + 6, u + 6, 4, 5, 0, comm, s);   // kept, blocks, stream_bytes, field_bytes
-  r |= ar(u + 10, u + 10, 1, 5, 2, comm, s); // status (bit flags: max of small ints ~ or)
+  r |= ar(u + 10, u + 10, 1, 5, 0, comm, s); // status lanes (sum)
   r |= ge();
   if (r) return fail(ISF_E_TASK_FAILED, "ncclAllReduce failed (%d)", r);
+  status_lanes_kernel<<<1, 1, 0, s>>>(u + 10, 1);
+  CUDA_TRY(cudaGetLastError());
   return 0;
 }
 

@@ -239,3 +239,34 @@ def test_determinism_stress(native, oracle, kind):
             assert np.array_equal(s, ref), f"stream differs on run {it}"
             assert np.array_equal(d, refd), f"reconstruction differs on run {it}"
             assert (rep.err2, rep.nrm2, rep.err_inf, rep.u_inf) == (refrep.err2, refrep.nrm2, refrep.err_inf, refrep.u_inf)
+
+
+def test_c_abi_allreduce_single_rank(native):
+    """isf_lossy_allreduce over a 1-rank NCCL communicator: sums/max are identities
+    and every status bit survives the lane spread/fold (NCCL has no OR)."""
+    import ctypes
+    import glob
+    import os
+    from paper_2407_20731_b200 import _native
+    libs = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "nccl", "lib", "libnccl.so*"))
+    if not libs:
+        pytest.skip("no libnccl")
+    nccl = ctypes.CDLL(libs[0], mode=ctypes.RTLD_GLOBAL)
+    comm = ctypes.c_void_p()
+    torch.cuda.set_device(0)
+    assert nccl.ncclCommInitAll(ctypes.byref(comm), 1, (ctypes.c_int * 1)(0)) == 0
+    try:
+        L = _native.lib()
+        for status in (0, 1, 2, 5, 7):
+            st = torch.zeros(12, dtype=torch.float64)
+            st[:6] = torch.tensor([1.5, 2.0, 0.25, 3.0, 0.125, 4.0], dtype=torch.float64)
+            st = st.cuda()
+            su = st.view(torch.int64)
+            su[6:11] = torch.tensor([11, 22, 33, 44, status], dtype=torch.int64, device="cuda")
+            ref = st.clone()
+            s = torch.cuda.current_stream()
+            assert L.isf_lossy_allreduce(ctypes.c_void_p(st.data_ptr()), comm, ctypes.c_void_p(s.cuda_stream)) == 0
+            torch.cuda.synchronize()
+            assert torch.equal(st.view(torch.int64)[:11], ref.view(torch.int64)[:11]), status
+    finally:
+        nccl.ncclCommDestroy(comm)
