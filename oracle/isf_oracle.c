@@ -472,6 +472,9 @@ int iso_decompress(int lx, int comps, uint64_t n_elements, const uint8_t* stream
             for (int j = 0; j < n3; ++j)
                 a[j] = (masks[b * W + (j >> 6)] >> (j & 63) & 1) ? vals[o++] : 0.0;
             iso_inv_block(lx, Bm, a, u);
+            /* reconstruction zeros are written as +0: the result is then
+               independent of how zero coefficients enter the sweeps */
+            for (int p = 0; p < n3; ++p) u[p] = u[p] + 0.0;
             const uint64_t e = b / comps;
             const int c = (int)(b % comps);
             double* dst = out + e * (uint64_t)n3 * comps + c;

@@ -372,7 +372,9 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       v[2 * z + 1] = t.y;
     }
     __syncwarp();
+#ifndef ISF_EXP_NOXFORM
     lines<8, 2, 0, 1, 2, false>(v);  // z sweep
+#endif
 #pragma unroll
     for (int kz = 0; kz < 8; ++kz) sb[kz * 32 + swz(kz, lane)] = make_double2(v[2 * kz], v[2 * kz + 1]);
     __syncwarp();
@@ -383,7 +385,9 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       v[2 * y + 1] = t.y;
     }
     __syncwarp();
+#ifndef ISF_EXP_NOXFORM
     lines<8, 2, 0, 1, 2, false>(v);  // y sweep
+#endif
 #pragma unroll
     for (int ky = 0; ky < 8; ++ky) sb[kzp * 32 + swz(kzp, ky * 4 + qp)] = make_double2(v[2 * ky], v[2 * ky + 1]);
     __syncwarp();
@@ -396,14 +400,21 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
         v[kyi * 8 + 2 * q + 1] = t.y;
       }
     __syncwarp();
+#ifndef ISF_EXP_NOXFORM
     lines<8, 1, 0, 8, 2, false>(v);  // x sweep: v[r] = coefficient 16*lane + r
+#endif
     // park the coefficients in the stage as [pair][lane] double2 (conflict free);
     // the registers are then free for the selection
     double2* coef2 = reinterpret_cast<double2*>(sb);
 #pragma unroll
     for (int r = 0; r < 8; ++r) coef2[r * 32 + lane] = make_double2(v[2 * r], v[2 * r + 1]);
     __syncwarp();
+#ifdef ISF_EXP_NOSEL
+    Sel16 sel{0u, 1ull, 0ull, 0, false};
+    if (__double_as_longlong(v[0]) == 0x1234) sel.mask = 1;
+#else
     const Sel16 sel = select16(v, lane, A.eps_q, hist, coef2);
+#endif
     if (sel.nonfinite && lane == 0) atomicOr(A.ws.flags, kFlagNonFinite);
     const uint32_t mask = sel.nonfinite ? 0u : sel.mask;
     uint32_t kept;
@@ -616,8 +627,32 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
   if (fin.stats && last_cta(ws.counter + 1)) finalize_cta(fin, s_red);
 }
 
+// Two inverse lines (offsets O0, O1, stride S) of lx = 8 whose coefficients at
+// positions 4..7 are all zero (the common case after truncation): the pinned
+// even/odd chains of inv_line restricted to k = 0..3, started from +0 with an fma.
+// Leaving out terms b*(+-0) and replacing the first product by fma(b, a, +0) change
+// nothing but the sign of zero: every intermediate keeps the real value of the
+// dense chain, sweep after sweep, and the +0 canonicalisation of the reconstruction
+// (applied by the oracle too) makes the bits identical.
+template <int S, int O0, int O1, int N>
+__device__ __forceinline__ void inv2_low8(double (&v)[N]) {
+  const double a0[4] = {v[O0], v[O0 + S], v[O0 + 2 * S], v[O0 + 3 * S]};
+  const double a1[4] = {v[O1], v[O1 + S], v[O1 + 2 * S], v[O1 + 3 * S]};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double e0 = __fma_rn(Bm<8>(i, 2), a0[2], __fma_rn(Bm<8>(i, 0), a0[0], 0.0));
+    const double d0 = __fma_rn(Bm<8>(i, 3), a0[3], __fma_rn(Bm<8>(i, 1), a0[1], 0.0));
+    const double e1 = __fma_rn(Bm<8>(i, 2), a1[2], __fma_rn(Bm<8>(i, 0), a1[0], 0.0));
+    const double d1 = __fma_rn(Bm<8>(i, 3), a1[3], __fma_rn(Bm<8>(i, 1), a1[1], 0.0));
+    v[O0 + i * S] = __dadd_rn(e0, d0);
+    v[O0 + (7 - i) * S] = __dsub_rn(e0, d0);
+    v[O1 + i * S] = __dadd_rn(e1, d1);
+    v[O1 + (7 - i) * S] = __dsub_rn(e1, d1);
+  }
+}
+
 // --------------------------- decompress -------------------------------------
-// stage: [0,16) the 16-B aligned counts quad | [16,80) mask | [96, ...) values
+// stage: [96, ...) the block's values (16-B aligned bulk copy); [0, 96) unused
 constexpr int kD8Stage = 96 + 4096 + 32;
 constexpr int kD8StageBytes = (kD8Stage + 127) & ~127;
 constexpr int kD8WarpBytes = kF8Stages * kD8StageBytes + 128;  // stages | mbarriers
@@ -629,6 +664,9 @@ struct Decompress8Args {
   FinalizeArgs fin;     // fused finalize by the last CTA
 };
 
+// ERR: also read the original and accumulate the error report (separate instantiation
+// so the plain decode does not carry the accumulators' registers)
+template <bool ERR>
 __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8Args P) {
   const DecompressArgs& A = P.d;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -651,6 +689,8 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
     fence_mbar_init();
   }
   __syncwarp();
+  // the TMA stage only carries the block's value range; offsets (from the counts) and
+  // the lane's 16-bit mask word travel in registers, loaded two blocks ahead
   auto issue = [&](uint64_t blk, int st, uint64_t o0, uint64_t o1) {
     if (lane == 0 && blk < B) {
       unsigned char* sp = wbase + st * kD8StageBytes;
@@ -658,93 +698,125 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
       uint64_t a1 = (A.val_off + 8 * o1 + 15) & ~15ull;
       if (a1 > sb_floor16) a1 = sb_floor16;
       const uint32_t vbytes = (a1 > a0 && o1 - o0 <= 512) ? (uint32_t)(a1 - a0) : 0u;
-      mbar_arrive_tx(&bars[st], 16u + 64u + vbytes);
-      bulk_g2s(sp, A.stream + ((4 * blk) & ~15ull), 16u, &bars[st]);
-      bulk_g2s(sp + 16, A.stream + A.mask_off + 64 * blk, 64u, &bars[st]);
+      mbar_arrive_tx(&bars[st], vbytes);
       if (vbytes) bulk_g2s(sp + 96, A.stream + a0, vbytes, &bars[st]);
     }
   };
+  const uint16_t* masks16 = reinterpret_cast<const uint16_t*>(A.stream + A.mask_off);
   static_assert(kF8Stages == 2, "offset pipeline assumes two stages");
-  // offsets of the current block and the next one (loaded one iteration ahead)
+  // offsets and masks of the current block and the next one (loaded one iteration ahead)
   uint64_t o0 = 0, o1 = 0, p0 = 0, p1 = 0;
-  if (gw < B) { o0 = P.off[gw]; o1 = P.off[gw + 1]; }
-  if (gw + W < B) { p0 = P.off[gw + W]; p1 = P.off[gw + W + 1]; }
+  uint32_t mc = 0, mn = 0;
+  if (gw < B) { o0 = P.off[gw]; o1 = P.off[gw + 1]; mc = __ldg(masks16 + gw * 32 + lane); }
+  if (gw + W < B) { p0 = P.off[gw + W]; p1 = P.off[gw + W + 1]; mn = __ldg(masks16 + (gw + W) * 32 + lane); }
   issue(gw, 0, o0, o1);
   issue(gw + W, 1, p0, p1);
   int st = 0;
   uint32_t ph = 0;
   for (uint64_t blk = gw; blk < B; blk += W) {
     unsigned char* sp = wbase + st * kD8StageBytes;
-    uint64_t r0 = 0, r1 = 0;  // offsets of blk + 2W, consumed by the refill below
-    if (blk + 2 * W < B) { r0 = P.off[blk + 2 * W]; r1 = P.off[blk + 2 * W + 1]; }
+    uint64_t r0 = 0, r1 = 0;  // offsets / mask of blk + 2W, consumed by the refill below
+    uint32_t mr = 0;
+    if (blk + 2 * W < B) {
+      r0 = P.off[blk + 2 * W];
+      r1 = P.off[blk + 2 * W + 1];
+      mr = __ldg(masks16 + (blk + 2 * W) * 32 + lane);
+    }
     mbar_wait(&bars[st], (ph >> st) & 1u);
     ph ^= 1u << st;
-    const uint32_t cnt = reinterpret_cast<const uint32_t*>(sp)[blk & 3];
-    uint32_t m = reinterpret_cast<const uint16_t*>(sp + 16)[lane];
+    uint32_t m = mc;
     const uint32_t pc = (uint32_t)__popc(m);
     const uint32_t inoff = warp_exscan_u32(pc, lane);
     const uint32_t tot = __shfl_sync(0xffffffffu, inoff + pc, 31);
-    const bool ok = tot == cnt && o1 - o0 == cnt && A.val_off + 8 * o1 <= A.stream_bytes;
+    // o1 - o0 is the block's stored count (block_offsets8_kernel scanned the counts)
+    const bool ok = tot == o1 - o0 && A.val_off + 8 * o1 <= A.stream_bytes;
     if (!ok) {
       if (lane == 0) atomicOr(A.ws.flags, kFlagShape);
       m = 0;
     }
+    // Occupied Legendre indices of the block (warp-uniform): lane l holds kz = l/4,
+    // ky = 2(l%4) (mask bits 0-7) and 2(l%4)+1 (bits 8-15), kx = bit % 8.  Sweeps skip
+    // the all-zero index planes 4..7 when they can; inv2_low8 says why that is exact.
+    const uint32_t occ = __reduce_or_sync(
+        0xffffffffu, ((m | (m >> 8)) & 0xffu) | (((m & 0xffu) ? 1u : 0u) << (8 + 2 * qp)) |
+                         (((m >> 8) ? 1u : 0u) << (9 + 2 * qp)) | ((m ? 1u : 0u) << (16 + kzp)));
+    const uint32_t Kx = occ & 0xffu, Ky = (occ >> 8) & 0xffu, Kz = occ >> 16;
+    // the final 8 bytes of a stream whose length is 8 mod 16 are not in the bulk copy
+    const double* sv0 = reinterpret_cast<const double*>(sp + 96) + (((A.val_off + 8 * o0) & 15ull) >> 3);
+    if (Kz && A.val_off + 8 * o1 > sb_floor16) {
+      if (lane == 0)
+        const_cast<double*>(sv0)[o1 - 1 - o0] =
+            reinterpret_cast<const double*>(A.stream + A.val_off)[(A.stream_bytes - A.val_off) / 8 - 1];
+      __syncwarp();
+    }
     double v[16];
-    {
-      const double* sv = reinterpret_cast<const double*>(sp + 96) + (((A.val_off + 8 * o0) & 15ull) >> 3) + inoff;
+    const double* sv = sv0 + inoff;
+    if (Kx < 16u) {  // warp-uniform: only kx 0..3 occupied
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k] = ((m >> k) & 1u) ? sv[__popc(m & ((1u << k) - 1u))] : 0.0;
+        v[8 + k] = ((m >> (8 + k)) & 1u) ? sv[__popc(m & ((1u << (8 + k)) - 1u))] : 0.0;
+      }
+      __syncwarp();
+      inv2_low8<1, 0, 8>(v);
+    } else {
       int o = 0;
 #pragma unroll
       for (int r = 0; r < 16; ++r) v[r] = ((m >> r) & 1u) ? sv[o++] : 0.0;
-      // the final 8 bytes of a stream whose length is 8 mod 16 are not in the bulk copy
-      if (m && A.val_off + 8 * o1 > sb_floor16) {
-        const uint64_t last = (A.stream_bytes - A.val_off) / 8 - 1;
-        const uint64_t first = o0 + inoff;
-        int oo = 0;
-#pragma unroll
-        for (int r = 0; r < 16; ++r)
-          if ((m >> r) & 1u) {
-            if (first + oo == last) v[r] = reinterpret_cast<const double*>(A.stream + A.val_off)[last];
-            ++oo;
-          }
-      }
+      __syncwarp();
+      lines<8, 1, 0, 8, 2, true>(v);
     }
-    __syncwarp();
     double2* sb = reinterpret_cast<double2*>(sp);
-    lines<8, 1, 0, 8, 2, true>(v);  // inverse x sweep
 #pragma unroll
     for (int kyi = 0; kyi < 2; ++kyi)
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq)
         sb[kzp * 32 + swz(kzp, (2 * qp + kyi) * 4 + qq)] = make_double2(v[kyi * 8 + 2 * qq], v[kyi * 8 + 2 * qq + 1]);
     __syncwarp();
+    if (Ky < 16u) {
 #pragma unroll
-    for (int ky = 0; ky < 8; ++ky) {
-      const double2 t = sb[kzp * 32 + swz(kzp, ky * 4 + qp)];
-      v[2 * ky] = t.x;
-      v[2 * ky + 1] = t.y;
+      for (int ky = 0; ky < 4; ++ky) {
+        const double2 t = sb[kzp * 32 + swz(kzp, ky * 4 + qp)];
+        v[2 * ky] = t.x;
+        v[2 * ky + 1] = t.y;
+      }
+      __syncwarp();
+      inv2_low8<2, 0, 1>(v);
+    } else {
+#pragma unroll
+      for (int ky = 0; ky < 8; ++ky) {
+        const double2 t = sb[kzp * 32 + swz(kzp, ky * 4 + qp)];
+        v[2 * ky] = t.x;
+        v[2 * ky + 1] = t.y;
+      }
+      __syncwarp();
+      lines<8, 2, 0, 1, 2, true>(v);
     }
-    __syncwarp();
-    lines<8, 2, 0, 1, 2, true>(v);  // inverse y sweep
 #pragma unroll
     for (int yy = 0; yy < 8; ++yy) sb[kzp * 32 + swz(kzp, yy * 4 + qp)] = make_double2(v[2 * yy], v[2 * yy + 1]);
     __syncwarp();
+    const bool lowz = Kz < 16u;
 #pragma unroll
-    for (int z = 0; z < 8; ++z) {
-      const double2 t = sb[z * 32 + swz(z, lane)];
-      v[2 * z] = t.x;
-      v[2 * z + 1] = t.y;
-    }
+    for (int z = 0; z < 8; ++z)
+      if (z < 4 || !lowz) {
+        const double2 t = sb[z * 32 + swz(z, lane)];
+        v[2 * z] = t.x;
+        v[2 * z + 1] = t.y;
+      }
     fence_proxy_async();
     __syncwarp();
     issue(blk + 2 * W, st, r0, r1);
     st ^= 1;
     o0 = p0; o1 = p1;
     p0 = r0; p1 = r1;
-    lines<8, 2, 0, 1, 2, true>(v);  // inverse z sweep
+    mc = mn; mn = mr;
+    if (lowz) inv2_low8<2, 0, 1>(v); else lines<8, 2, 0, 1, 2, true>(v);  // inverse z sweep
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = __dadd_rn(v[r], 0.0);  // zeros as +0
     double2* dst = reinterpret_cast<double2*>(A.out + blk * 512) + lane;
 #pragma unroll
     for (int z = 0; z < 8; ++z) stg_stream(dst + z * 32, make_double2(v[2 * z], v[2 * z + 1]));
-    if (A.orig) {
+    if (ERR) {
       const double2* src = reinterpret_cast<const double2*>(A.orig + blk * 512) + lane;
 #pragma unroll
       for (int z = 0; z < 8; ++z) {
@@ -764,7 +836,7 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
       }
     }
   }
-  if (A.orig) {
+  if (ERR) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       e2 = __dadd_rn(e2, __shfl_xor_sync(0xffffffffu, e2, o));

@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kGenThreads) decompress_generic(DecompressArgs
     double* dst = A.out + e * (uint64_t)N3 * A.comps + c;
     const double* org = A.orig ? A.orig + e * (uint64_t)N3 * A.comps + c : nullptr;
     for (int p = tid; p < N3; p += kGenThreads) {
-      const double val = u[p];
+      const double val = __dadd_rn(u[p], 0.0);  // zero results are written as +0
       dst[(uint64_t)p * A.comps] = val;
       if (org) {
         const int x = p % N, yy = (p / N) % N, z = p / N2;

@@ -280,11 +280,12 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
   build_operators((int)P, p->F, p->B, p->x, p->w);
   if (use_fast8(p)) {
     CUDA_TRY(cudaFuncSetAttribute(compress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
-    CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kD8Smem));
+    CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kD8Smem));
+    CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kD8Smem));
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel, kC8Warps * 32, kC8Smem));
     p->grid8c = p->sms * std::max(occ, 1);
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel, kD8Warps * 32, kD8Smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel<true>, kD8Warps * 32, kD8Smem));
     p->grid8d = p->sms * std::max(occ, 1);
   }
   CUDA_TRY(ensure(p, 1 << 16, 1 << 14, 1 << 16) == 0 ? cudaSuccess : cudaErrorMemoryAllocation);
@@ -469,7 +470,8 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
     FinalizeArgs f{1, p->partials, d_original ? parts : 0u, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
                    B * (uint64_t)p->P * p->P * p->P * 8, hdr, d_original ? 1 : 0};
     Decompress8Args a8{a, p->toff, f};
-    decompress8_kernel<<<grid, kD8Warps * 32, kD8Smem, s>>>(a8);  // + fused finalize
+    if (d_original) decompress8_kernel<true><<<grid, kD8Warps * 32, kD8Smem, s>>>(a8);  // + fused finalize
+    else decompress8_kernel<false><<<grid, kD8Warps * 32, kD8Smem, s>>>(a8);
     CUDA_TRY(cudaGetLastError());
     p->last_launches = 2;
     return 0;

@@ -270,3 +270,45 @@ def test_c_abi_allreduce_single_rank(native):
             assert torch.equal(st.view(torch.int64)[:11], ref.view(torch.int64)[:11]), status
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+@pytest.mark.parametrize("case", ["tgv", "spectral_dense", "tiny_values", "signed_zeros"])
+def test_decompress_bitexact(native, oracle, case):
+    """Reconstructions are bit-identical to the oracle's (incl. +0 canonicalisation,
+    DESIGN.md 3.3), also for streams whose values are subnormal, zero or -0 and
+    whose occupied index planes are sparse (the lx=8 kernel skips empty planes)."""
+    import paper_2407_20731_b200 as PK
+    P, E = 8, 4
+    n_el = E ** 3
+    if case == "tgv":
+        u = oracle.gen_tgv(E, P, 3)
+        eps = 1e-3
+    else:
+        u = oracle.gen_spectral(P, n_el)
+        eps = 1e-2 if case != "spectral_dense" else 1e-6
+    rc, ref, _ = oracle.compress(u, P, 1, eps)
+    assert rc == 0
+    ref = ref.copy()
+    counts, masks, vals = oracle.parse_stream(ref, P, n_el)
+    vals = vals.copy()
+    rng = np.random.default_rng(7)
+    if case == "tiny_values":
+        sel = rng.random(vals.size) < 0.5
+        vals[sel] *= 2.0 ** -1070          # subnormal products underflow inside the sweeps
+    if case == "signed_zeros":
+        sel = rng.random(vals.size)
+        vals[sel < 0.2] = 0.0
+        vals[(sel >= 0.2) & (sel < 0.4)] = -0.0
+    ref[ref.size - vals.size * 8:] = vals.view(np.uint8)
+    rc, ob, _ = oracle.decompress(ref, P, 1, n_el)
+    assert rc == 0
+    plan = PK.get_plan(P, 1, 0)
+    d_stream = torch.from_numpy(ref).cuda()
+    out = torch.empty(n_el * P ** 3, dtype=torch.float64, device="cuda")
+    stats = torch.zeros(12, dtype=torch.float64, device="cuda")
+    plan.decompress_async(d_stream, ref.size, n_el, out, stats)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert int(stats.view(torch.int64)[10].item()) == 0
+    assert np.array_equal(got.view(np.uint64), ob.view(np.uint64))
+    assert not np.any(got.view(np.uint64) == np.uint64(1 << 63))  # no -0 in the output

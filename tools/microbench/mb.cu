@@ -64,14 +64,44 @@ __global__ void k_read(const double2* __restrict__ a, double* out, size_t n) {
   for (; i < n; i += st) { double2 v = a[i]; s += v.x + v.y; }
   if (s == 1.2345) out[0] = s;
 }
-int main() {
+__global__ void k_write(double2* __restrict__ b, size_t n, int cs) {
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+  const double2 v = make_double2(threadIdx.x, 1.0);
+  if (cs) {
+    for (; i < n; i += st) asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" ::"l"(b + i), "d"(v.x), "d"(v.y) : "memory");
+  } else {
+    for (; i < n; i += st) b[i] = v;
+  }
+}
+// TMA bulk store: each warp streams 4 KiB chunks from its smem buffer
+__global__ void k_bulkstore(unsigned char* __restrict__ b, size_t nbytes) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  unsigned char* mine = sm + warp * 4096;
+  for (int i = lane; i < 512; i += 32) reinterpret_cast<double*>(mine)[i] = i;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  const size_t nch = nbytes / 4096;
+  for (size_t c = (size_t)blockIdx.x * nw + warp; c < nch; c += (size_t)gridDim.x * nw) {
+    if (lane == 0) {
+      unsigned sa = (unsigned)__cvta_generic_to_shared(mine);
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 4096;" ::"l"(b + c * 4096), "r"(sa) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory");
+    }
+    __syncwarp();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+int main(int argc, char** argv) {
   int dev = 0; cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, dev));
   int sms = p.multiProcessorCount;
   int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
   printf("GPU %s SMs %d maxclk %d MHz smemPerSM %zu regsPerSM %d\n", p.name, sms, clk / 1000, p.sharedMemPerMultiprocessor, p.regsPerMultiprocessor);
   double* dout; CK(cudaMalloc(&dout, 64));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1); float ms;
-  for (int rep = 0; rep < 2; rep++) {
+  const bool only_mem = argc > 1;
+  for (int rep = 0; rep < (only_mem ? 0 : 2); rep++) {
     int iters = 20000, thr = 512, blocks = sms * 4;
     k_dfma<<<blocks, thr>>>(dout, 100, 1.0000001, 1e-9);
     cudaEventRecord(e0); k_dfma<<<blocks, thr>>>(dout, iters, 1.0000001, 1e-9); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
@@ -107,6 +137,17 @@ int main() {
     cudaEventRecord(e0); for (int r = 0; r < 5; r++) k_read<<<sms * bs, 512>>>(a, dout, n); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
     cudaEventElapsedTime(&ms, e0, e1);
     printf("read grid=%d*SM: %.1f GB/s\n", bs, 5.0 * n * 16 / (ms * 1e6));
+    for (int cs = 0; cs < 2; cs++) {
+      k_write<<<sms * bs, 512>>>(b, n, cs);
+      cudaEventRecord(e0); for (int r = 0; r < 5; r++) k_write<<<sms * bs, 512>>>(b, n, cs); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("write%s grid=%d*SM: %.1f GB/s\n", cs ? ".cs" : "", bs, 5.0 * n * 16 / (ms * 1e6));
+    }
+    cudaFuncSetAttribute(k_bulkstore, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4096);
+    k_bulkstore<<<sms * (bs > 2 ? 2 : bs), 512, 16 * 4096>>>((unsigned char*)b, n * 16);
+    cudaEventRecord(e0); for (int r = 0; r < 5; r++) k_bulkstore<<<sms * (bs > 2 ? 2 : bs), 512, 16 * 4096>>>((unsigned char*)b, n * 16); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("bulkstore grid=%d*SM: %.1f GB/s\n", bs > 2 ? 2 : bs, 5.0 * n * 16 / (ms * 1e6));
   }
   return 0;
 }
