@@ -137,6 +137,25 @@ int isf_lossy_decompress_host(isf_lossy_plan* plan, const void* h_stream, uint64
  * link-time NCCL dependency and uses whichever NCCL created the communicator. */
 int isf_lossy_allreduce(isf_lossy_stats* d_stats, void* nccl_comm, void* cuda_stream);
 
+/* Device CRC-32 (IEEE / zlib polynomial; replaces the host zlib call of
+ * proj/src/core/crc32.cpp:7-20 for device-resident data): *d_crc = crc32(d_data[0..n)).
+ * Asynchronous on cuda_stream; any alignment (16-byte aligned data takes the fast path). */
+int isf_lossy_crc32(isf_lossy_plan* plan, const void* d_data, uint64_t n, uint32_t* d_crc,
+                    void* cuda_stream);
+
+/* Kind-1 frame on the device (proj/include/isf/core/frame.hpp:3-11,
+ * proj/src/core/frame.cpp:9-25 build_frame, SPEC.md:282 payload):
+ *   [0,48) header "ISF1" | 1 | kind 1 | step | sim_time | E | P | components | 0 | payload_len
+ *   [48, 48+S) the stream, which the caller has compressed in place (d_stream = d_frame + 48)
+ *   codec id u16 = 0 | coded length u64 = 0 (no lossless stage) | CRC-32 u32 of all preceding bytes
+ * S is read from d_stats->stream_bytes (the stats of that compress call), so the call is
+ * fully asynchronous; the frame is S + ISF_FRAME_OVERHEAD bytes.  d_frame is 16-byte
+ * aligned; a frame_cap that is too small sets ISF_STATUS_OVERFLOW in d_stats->status. */
+#define ISF_FRAME_OVERHEAD 62
+int isf_lossy_frame_async(isf_lossy_plan* plan, void* d_frame, uint64_t frame_cap,
+                          const isf_lossy_stats* d_stats, uint32_t elements_per_axis,
+                          uint64_t step_index, double sim_time, void* cuda_stream);
+
 /* Eq. 1: (original - compressed) / original in fp64. */
 double isf_lossy_compression_ratio(uint64_t original_size, uint64_t compressed_size);
 

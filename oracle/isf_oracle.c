@@ -618,5 +618,6 @@ void iso_gen_spectral(int lx, uint64_t block0, uint64_t nblocks, uint64_t seed, 
             a[j] = U2 * amp[j];
         }
         iso_inv_block(lx, Bm, a, out + b * n3);
+        for (int j = 0; j < n3; ++j) out[b * n3 + j] += 0.0; /* zeros as +0, like decompress */
     }
 }

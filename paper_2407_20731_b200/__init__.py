@@ -9,6 +9,6 @@ interface.  See DESIGN.md.
 from .lossy import (  # noqa: F401
     CompressedBlock, CompressionReport, ErrorCode, ErrorNorm, ErrorReport, Field, IsfError,
     LossyConfig, LossyPlan, compression_ratio, decompress_with_error, get_plan, lossy_compress,
-    lossy_decompress,
+    lossy_compress_frame, lossy_decompress,
 )
 from ._native import LIB_PATH, EXPORTS  # noqa: F401

@@ -21,8 +21,9 @@ EXPORTS = (
     "isf_lossy_decompress_host", "isf_lossy_allreduce", "isf_lossy_compression_ratio",
     "isf_lossy_last_error", "isf_lossy_error_code_name", "isf_lossy_plan_operators",
     "isf_lossy_plan_last_launches", "isf_lossy_generate_tgv", "isf_lossy_generate_spectral",
-    "isf_lossy_solver_standin",
+    "isf_lossy_solver_standin", "isf_lossy_crc32", "isf_lossy_frame_async",
 )
+FRAME_OVERHEAD = 62  # ISF_FRAME_OVERHEAD: 48-B header + codec trailer (10 B) + CRC (4 B)
 
 
 class Stats(ctypes.Structure):
@@ -73,6 +74,8 @@ def lib() -> ctypes.CDLL:
         "isf_lossy_generate_tgv": ([P, P, u32, u32, u32, i32, f64, P], i32),
         "isf_lossy_generate_spectral": ([P, P, u64, u64, u64, P, P], i32),
         "isf_lossy_solver_standin": ([P, P, P, u64, f64, P], i32),
+        "isf_lossy_crc32": ([P, P, u64, P, P], i32),
+        "isf_lossy_frame_async": ([P, P, u64, P, u32, u64, f64, P], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

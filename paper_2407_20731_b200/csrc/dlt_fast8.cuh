@@ -215,10 +215,19 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
     const double2 t = coef2[(r >> 1) * 32 + lane];
     return (r & 1) ? t.y : t.x;
   };
+#ifdef ISF_OPT_DMAX
+  // max |a| by fp64 max (NaN-ignoring); a non-finite input makes every coefficient of
+  // the lx=8 block non-finite (no zero in F), so the lane maximum is Inf or NaN then
+  double am = fmax(fabs(v[0]), fabs(v[1]));
+#pragma unroll
+  for (int r = 2; r < 16; ++r) am = fmax(am, fabs(v[r]));
+  uint32_t hm = __reduce_max_sync(0xffffffffu, (uint32_t)__double2hiint(am));
+#else
   uint32_t hm = 0;
 #pragma unroll
   for (int r = 0; r < 16; ++r) hm = ::max(hm, (uint32_t)__double2hiint(v[r]) & 0x7fffffffu);
   hm = __reduce_max_sync(0xffffffffu, hm);
+#endif
   if (hm >= 0x7ff00000u) { s.nonfinite = true; return s; }
   int sexp;
   if (hm >= 0x00100000u) {
@@ -249,8 +258,13 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
 #pragma unroll
   for (int r = 0; r < 16; r += 2) {
     const double xa = __dmul_rn(v[r], f), xb = __dmul_rn(v[r + 1], f);
+#ifdef ISF_OPT_FMARD
+    t[r] = __fma_rd(xa, xa, 4503599627370496.0);
+    t[r + 1] = __fma_rd(xb, xb, 4503599627370496.0);
+#else
     t[r] = __dadd_rd(__dmul_rn(xa, xa), 4503599627370496.0);
     t[r + 1] = __dadd_rd(__dmul_rn(xb, xb), 4503599627370496.0);
+#endif
     t0 += (uint64_t)__double_as_longlong(t[r]);
     t1 += (uint64_t)__double_as_longlong(t[r + 1]);
   }
@@ -261,11 +275,29 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   const double tthr = 4503599627370496.0 + (double)(thr < (1ull << 51) ? thr : (1ull << 51));
   uint32_t mH = 0;
   uint64_t h0 = 0, h1s = 0;
+#ifdef ISF_OPT_FUSEMAX
+  double tmd = 0.0;  // largest t outside H (for the one-move path)
+#pragma unroll
+  for (int r = 0; r < 16; r += 2) {
+    if (t[r] >= tthr) { mH |= 1u << r; h0 += (uint64_t)__double_as_longlong(t[r]); } else tmd = fmax(tmd, t[r]);
+    if (t[r + 1] >= tthr) { mH |= 1u << (r + 1); h1s += (uint64_t)__double_as_longlong(t[r + 1]); } else tmd = fmax(tmd, t[r + 1]);
+  }
+#elif defined(ISF_OPT_HINT)
+  // integer classification (keeps the FP64 pipe free): t >= tthr <=> bits(t) >= bits(tthr)
+  const uint64_t tthr_b = C52 + (thr < (1ull << 51) ? thr : (1ull << 51));
+#pragma unroll
+  for (int r = 0; r < 16; r += 2) {
+    const uint64_t ba = (uint64_t)__double_as_longlong(t[r]), bb = (uint64_t)__double_as_longlong(t[r + 1]);
+    if (ba >= tthr_b) { mH |= 1u << r; h0 += ba; }
+    if (bb >= tthr_b) { mH |= 1u << (r + 1); h1s += bb; }
+  }
+#else
 #pragma unroll
   for (int r = 0; r < 16; r += 2) {
     if (t[r] >= tthr) { mH |= 1u << r; h0 += (uint64_t)__double_as_longlong(t[r]); }
     if (t[r + 1] >= tthr) { mH |= 1u << (r + 1); h1s += (uint64_t)__double_as_longlong(t[r + 1]); }
   }
+#endif
   const uint32_t nH = (uint32_t)__popc(mH);
   const uint64_t SH = warp_sum_u58(h0 + h1s - nH * C52);  // sum of lo over H
   const uint32_t NH = __reduce_add_sync(0xffffffffu, nH);
@@ -279,6 +311,9 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   // index among ties) joins the kept set if that suffices.
   // t is monotone in |a|: the largest t among the non-kept gives the candidates (its
   // lo + 1 is the hi to move); ties in t are resolved by |a|, then the smallest index.
+#ifdef ISF_OPT_FUSEMAX
+  const uint64_t gtm = warp_max_u64((uint64_t)__double_as_longlong(tmd));
+#else
   uint64_t tm = 0;
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
@@ -286,6 +321,7 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
     tm = tb > tm ? tb : tm;
   }
   const uint64_t gtm = warp_max_u64(tm);
+#endif
   uint32_t cm = 0;
 #pragma unroll
   for (int r = 0; r < 16; ++r)

@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) 
   constexpr int N = LX, N2 = LX * LX, N3 = LX * LX * LX;
   constexpr int W = (N3 + 63) / 64;
   using L = GenSmem<LX>;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   double* u = reinterpret_cast<double*>(smem + L::u_off);
   uint64_t* ckeys = reinterpret_cast<uint64_t*>(smem + L::key_off);
   uint16_t* cidx = reinterpret_cast<uint16_t*>(smem + L::idx_off);
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kGenThreads) decompress_generic(DecompressArgs
   constexpr int N = LX, N2 = LX * LX, N3 = LX * LX * LX;
   constexpr int W = (N3 + 63) / 64;
   using L = GenSmem<LX>;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   double* u = reinterpret_cast<double*>(smem + L::u_off);
   uint64_t* maskw = reinterpret_cast<uint64_t*>(smem + L::mask_off);
   uint32_t* wpre = reinterpret_cast<uint32_t*>(smem + L::key_off);  // prefix popcounts per word

@@ -14,6 +14,7 @@
 
 #include "../../include/isf_lossy.h"
 #include "dlt_fast8.cuh"
+#include "crc32.cuh"
 
 namespace isf {
 namespace host {
@@ -62,6 +63,10 @@ int init_device_constants(int device) {
   CUDA_TRY(cudaMemcpyToSymbol(c_ops, ops, sizeof ops));
   CUDA_TRY(cudaMemcpyToSymbol(c_w, ws, sizeof ws));
   CUDA_TRY(cudaMemcpyToSymbol(c_x, xs, sizeof xs));
+  static isf::crc::Tables crc_tables;
+  static bool crc_built = false;
+  if (!crc_built) { isf::crc::build_tables(crc_tables); crc_built = true; }
+  CUDA_TRY(cudaMemcpyToSymbol(isf::crc::g_tables, &crc_tables, sizeof crc_tables));
   g_dev_init[device] = true;
   return 0;
 }
@@ -113,6 +118,10 @@ struct isf_lossy_plan {
   void* d_aux = nullptr;
   size_t d_aux_cap = 0;
   cudaStream_t host_stream = nullptr;
+  // device CRC / framing
+  uint32_t* crc_chunks = nullptr;
+  size_t crc_cap = 0;
+  uint64_t* crc_n = nullptr;
   int grid8c = 0, grid8d = 0, gridg = 0;
   size_t smem_g = 0;
 };
@@ -307,6 +316,8 @@ int isf_lossy_plan_destroy(isf_lossy_plan* p) {
   cudaFree(p->d_in);
   cudaFree(p->d_out);
   cudaFree(p->d_aux);
+  cudaFree(p->crc_chunks);
+  cudaFree(p->crc_n);
   if (p->host_stream) cudaStreamDestroy(p->host_stream);
   delete p;
   return 0;
@@ -568,6 +579,61 @@ int isf_lossy_decompress_host(isf_lossy_plan* p, const void* h_stream, uint64_t 
 }
 
 // ---- NCCL (resolved at run time) ----
+// ---------------------------------------------------------------------------
+// Device CRC-32 and kind-1 framing (crc32.cuh)
+// ---------------------------------------------------------------------------
+namespace {
+int crc_launch(isf_lossy_plan* p, const uint8_t* d, const uint64_t* n_dev, uint64_t n_max, uint32_t* out,
+               uint8_t* frame_tail, cudaStream_t s) {
+  const size_t nch = (size_t)((n_max + isf::crc::kChunk - 1) / isf::crc::kChunk) + 1;
+  if (nch > p->crc_cap) {
+    if (p->crc_chunks) cudaFree(p->crc_chunks);
+    const size_t cap = std::max<size_t>(nch, 4096);
+    CUDA_TRY(cudaMalloc(&p->crc_chunks, cap * sizeof(uint32_t)));
+    p->crc_cap = cap;
+  }
+  const uint64_t warps = std::max<uint64_t>(nch, 1);
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((warps + 7) / 8, (uint64_t)p->sms * 8);
+  isf::crc::crc_chunks_kernel<<<grid, 256, 0, s>>>(d, n_dev, n_max, p->crc_chunks);
+  CUDA_TRY(cudaGetLastError());
+  isf::crc::crc_final_kernel<<<1, isf::crc::kFinalThreads, 0, s>>>(p->crc_chunks, n_dev, n_max, out, frame_tail);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int isf_lossy_crc32(isf_lossy_plan* p, const void* d_data, uint64_t n, uint32_t* d_crc, void* cuda_stream) {
+  if (int rc = check_plan(p)) return rc;
+  if ((!d_data && n) || !d_crc) return fail(ISF_E_INVALID_ARGUMENT, "null data or output pointer");
+  DeviceGuard dg(p->device);
+  p->last_launches = 2;
+  return crc_launch(p, (const uint8_t*)d_data, nullptr, n, d_crc, nullptr, (cudaStream_t)cuda_stream);
+}
+
+int isf_lossy_frame_async(isf_lossy_plan* p, void* d_frame, uint64_t frame_cap, const isf_lossy_stats* d_stats,
+                          uint32_t elements_per_axis, uint64_t step_index, double sim_time, void* cuda_stream) {
+  if (int rc = check_plan(p)) return rc;
+  if (!d_frame || !d_stats) return fail(ISF_E_INVALID_ARGUMENT, "null frame or stats pointer");
+  if (((uintptr_t)d_frame & 15u) != 0) return fail(ISF_E_INVALID_ARGUMENT, "frame must be 16-byte aligned");
+  if (frame_cap < ISF_FRAME_OVERHEAD) return fail(ISF_E_LENGTH_MISMATCH, "frame capacity below %d bytes", ISF_FRAME_OVERHEAD);
+  DeviceGuard dg(p->device);
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  if (!p->crc_n) CUDA_TRY(cudaMalloc(&p->crc_n, 64));
+  isf::crc::frame_header_kernel<<<1, 32, 0, s>>>((uint8_t*)d_frame, frame_cap, &d_stats->stream_bytes,
+                                                 elements_per_axis, p->P, p->comps, step_index, sim_time, p->crc_n,
+                                                 reinterpret_cast<unsigned long long*>(
+                                                     const_cast<uint64_t*>(&d_stats->status)));
+  CUDA_TRY(cudaGetLastError());
+  if (int rc = crc_launch(p, (const uint8_t*)d_frame, p->crc_n, frame_cap - 4, nullptr, (uint8_t*)d_frame, s))
+    return rc;
+  p->last_launches = 3;
+  return 0;
+}
+
+}  // extern "C"
+
 namespace {
 __global__ void status_lanes_kernel(uint64_t* st, int fold) {
   const uint64_t v = *st;

@@ -289,6 +289,20 @@ class LossyPlan:
             ctypes.c_void_p(stream_buf.data_ptr()), stream_buf.numel(),
             ctypes.c_void_p(stats_buf.data_ptr()), ctypes.c_void_p(cs.cuda_stream)))
 
+    def crc32_async(self, data: torch.Tensor, nbytes: int, out: torch.Tensor, cuda_stream=None):
+        """Device CRC-32 (zlib) of the first nbytes of a CUDA tensor into out (int32/uint32[1])."""
+        cs = torch.cuda.current_stream(self.device) if cuda_stream is None else cuda_stream
+        _check(self._lib.isf_lossy_crc32(self._h, ctypes.c_void_p(data.data_ptr()), int(nbytes),
+                                         ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(cs.cuda_stream)))
+
+    def frame_async(self, frame_buf: torch.Tensor, stats_buf: torch.Tensor, elements_per_axis: int,
+                    step_index: int = 0, sim_time: float = 0.0, cuda_stream=None):
+        """Kind-1 frame around the stream compressed at frame_buf[48:] (stats_buf = that call's stats)."""
+        cs = torch.cuda.current_stream(self.device) if cuda_stream is None else cuda_stream
+        _check(self._lib.isf_lossy_frame_async(self._h, ctypes.c_void_p(frame_buf.data_ptr()), frame_buf.numel(),
+                                               ctypes.c_void_p(stats_buf.data_ptr()), int(elements_per_axis),
+                                               int(step_index), float(sim_time), ctypes.c_void_p(cs.cuda_stream)))
+
     def decompress_async(self, stream_buf: torch.Tensor, stream_bytes: int, n_elements: int,
                          out: torch.Tensor, stats_buf: torch.Tensor, original: torch.Tensor | None = None,
                          cuda_stream=None):
@@ -375,6 +389,38 @@ def lossy_compress(field: Field, cfg: LossyConfig, *, plan: LossyPlan | None = N
            "rel_l2_estimate": math.sqrt(st.disc2 / st.tot2) if st.tot2 > 0 else 0.0}
     return CompressedBlock(buf[: nb.value], n_el, field.points_per_element_axis, field.components,
                            int(st.kept), rep, estimate=est)
+
+
+def lossy_compress_frame(field: Field, cfg: LossyConfig, step_index: int = 0, sim_time: float = 0.0, *,
+                         plan: LossyPlan | None = None):
+    """Compress straight into a staging-ready kind-1 frame on the device:
+    header, stream, codec trailer and CRC-32 are all written by kernels, so the only
+    host work left is one D2H copy of the frame (StageWriter::write_frame,
+    proj/include/isf/staging/staging.hpp:59-60).  Returns (frame uint8 CUDA tensor of
+    exactly the frame bytes, CompressionReport, kept count)."""
+    field.validate_shape()
+    v = _device_values(field)
+    dev = v.device.index
+    plan = plan or get_plan(field.points_per_element_axis, field.components, dev)
+    n_el = field.element_count()
+    cap = plan.capacity(n_el) + _native.FRAME_OVERHEAD
+    frame = torch.empty(cap, dtype=torch.uint8, device=v.device)
+    stats = torch.zeros(12, dtype=torch.float64, device=v.device)
+    cs = torch.cuda.current_stream(dev)
+    _check(plan._lib.isf_lossy_compress_async(plan.handle, ctypes.c_void_p(v.data_ptr()), n_el,
+                                              float(cfg.max_error), int(cfg.error_norm),
+                                              ctypes.c_void_p(frame.data_ptr() + 48), cap - 48,
+                                              ctypes.c_void_p(stats.data_ptr()), ctypes.c_void_p(cs.cuda_stream)))
+    plan.frame_async(frame, stats, field.elements_per_axis, step_index, sim_time, cuda_stream=cs)
+    st = stats.view(torch.int64).cpu()
+    status = int(st[10])
+    if status & 1:
+        raise IsfError(ErrorCode.InvalidArgument, "Field: non-finite value (types.cpp:71-73)")
+    if status:
+        raise IsfError(ErrorCode.SerializationFailed, f"frame assembly failed (status {status})")
+    sb = int(st[8])
+    rep = CompressionReport.from_sizes(int(st[9]), sb)
+    return frame[: sb + _native.FRAME_OVERHEAD], rep, int(st[6])
 
 
 def _decompress(block: CompressedBlock, shape, original: torch.Tensor | None):
