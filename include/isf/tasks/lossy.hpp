@@ -39,8 +39,8 @@ struct LossyConfig {
     void validate() const {
         if (!(max_error > 0.0 && max_error < 1.0))
             throw Error(ErrorCode::InvalidArgument, "LossyConfig: max_error must be in (0,1)");
-        if (error_norm != ErrorNorm::RelativeL2)
-            throw Error(ErrorCode::InvalidArgument, "LossyConfig: only RelativeL2 truncation is implemented");
+        if (error_norm != ErrorNorm::RelativeL2 && error_norm != ErrorNorm::RelativeLInf)
+            throw Error(ErrorCode::InvalidArgument, "LossyConfig: unknown error_norm");
     }
 };
 

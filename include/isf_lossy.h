@@ -56,8 +56,10 @@ enum {
     ISF_E_INVALID_ARGUMENT = 1 + 20     /* ErrorCode::InvalidArgument     */
 };
 
-/* LossyConfig.error_norm.  v1 enforces RelativeL2; RelativeLInf is
- * rejected with ISF_E_INVALID_ARGUMENT (reported, not enforced: DESIGN.md 6). */
+/* LossyConfig.error_norm.  RelativeL2: exact Parseval energy rule
+ * (DESIGN.md 3.4).  RelativeLInf: per block, sum over the discarded coefficients of
+ * |a_j| * max|basis_j| <= max_error * max|u| (a bound on the reconstruction's max
+ * error; runs on the generic kernels). */
 enum { ISF_NORM_RELATIVE_L2 = 0, ISF_NORM_RELATIVE_LINF = 1 };
 
 /* status bits in isf_lossy_stats.status */

@@ -326,6 +326,87 @@ static void gather_block(int n3, int comps, const double* field, uint64_t e, int
     for (int p = 0; p < n3; ++p) out[p] = base[(uint64_t)p * comps];
 }
 
+/* ------------------------------------------------------------------------- */
+/* RelativeLInf rule:         */
+/*   bm_k = max_i |B[i][k]|,  Bmax_j = RU(RU(bm_kx bm_ky) bm_kz)               */
+/*   x_j  = RU(|a_j| Bmax_j),  m = max x_j = f 2^s (frexp),  k = KL - s,       */
+/*   KL   = 63 - ceil(log2 lx^3),  w_j = x_j == 0 ? 0 : max(1, ceil(x_j 2^k))  */
+/*   thr  = floor(RD(eps max|u|) 2^k)  (clamped to 2^63)                       */
+/*   discarded set = longest prefix of (|a| asc, index desc) with sum w <= thr */
+/* so that sum_discarded |a_j| Bmax_j <= eps max|u| >= max|u - u~| (exact      */
+/* arithmetic).  RU / RD products are exact via binary128.                     */
+/* ------------------------------------------------------------------------- */
+static double mul_ru(double x, double y) {
+    const __float128 q = (__float128)x * (__float128)y;
+    double p = (double)q;
+    if ((__float128)p < q) p = nextafter(p, INFINITY);
+    return p;
+}
+static double mul_rd(double x, double y) {
+    const __float128 q = (__float128)x * (__float128)y;
+    double p = (double)q;
+    if ((__float128)p > q) p = nextafter(p, -INFINITY);
+    return p;
+}
+
+uint32_t iso_select_block_linf(int lx, const double* Bm, const double* a, double umax, double max_error,
+                               uint64_t* mask, int* nonfinite) {
+    const int n3 = lx * lx * lx, W = (n3 + 63) / 64;
+    for (int w = 0; w < W; ++w) mask[w] = 0;
+    if (nonfinite) *nonfinite = 0;
+    double bm[ISO_MAX_LX];
+    for (int k = 0; k < lx; ++k) {
+        double m = 0.0;
+        for (int i = 0; i < lx; ++i) m = fmax(m, fabs(Bm[i * lx + k]));
+        bm[k] = m;
+    }
+    static __thread double x[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+    static __thread sel_item items[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+    double xm = 0.0;
+    for (int j = 0; j < n3; ++j) {
+        if (!isfinite(a[j])) {
+            if (nonfinite) *nonfinite = 1;
+            return 0;
+        }
+        const int kx = j % lx, ky = (j / lx) % lx, kz = j / (lx * lx);
+        x[j] = mul_ru(fabs(a[j]), mul_ru(mul_ru(bm[kx], bm[ky]), bm[kz]));
+        if (x[j] > xm) xm = x[j];
+        uint64_t b;
+        memcpy(&b, &a[j], 8);
+        items[j].key = b & 0x7fffffffffffffffull;
+        items[j].idx = j;
+    }
+    if (!isfinite(xm)) {
+        if (nonfinite) *nonfinite = 1;
+        return 0;
+    }
+    if (xm == 0.0) return 0; /* all-zero block keeps nothing */
+    int s;
+    (void)frexp(xm, &s);
+    const int k = (63 - ceil_log2_u32((uint32_t)n3)) - s;
+    const double tb = floor(ldexp(mul_rd(max_error, umax), k));
+    const uint64_t thr = tb >= 9223372036854775808.0 ? (1ull << 63) : (uint64_t)tb;
+    qsort(items, (size_t)n3, sizeof(sel_item), cmp_discard_order);
+    uint64_t acc = 0;
+    int m = 0;
+    while (m < n3) {
+        const double xj = x[items[m].idx];
+        uint64_t w = 0;
+        if (xj != 0.0) {
+            const double c = ceil(ldexp(xj, k));
+            w = c < 1.0 ? 1 : (uint64_t)c;
+        }
+        if (acc + w > thr) break;
+        acc += w;
+        ++m;
+    }
+    for (int p = m; p < n3; ++p) {
+        const int j = items[p].idx;
+        mask[j >> 6] |= 1ull << (j & 63);
+    }
+    return (uint32_t)(n3 - m);
+}
+
 static int omp_threads(int nthreads) {
 #ifdef _OPENMP
     return nthreads > 0 ? nthreads : omp_get_max_threads();
@@ -337,6 +418,12 @@ static int omp_threads(int nthreads) {
 
 int iso_compress(int lx, int comps, uint64_t n_elements, const double* field, double max_error,
                  uint8_t* stream, uint64_t cap, uint64_t* stream_bytes, iso_stats* st, int nthreads) {
+    return iso_compress_norm(lx, comps, n_elements, field, max_error, 0, stream, cap, stream_bytes, st, nthreads);
+}
+
+int iso_compress_norm(int lx, int comps, uint64_t n_elements, const double* field, double max_error, int norm,
+                      uint8_t* stream, uint64_t cap, uint64_t* stream_bytes, iso_stats* st, int nthreads) {
+    if (norm != 0 && norm != 1) return ERR_INVALID;
     if (lx < 2 || lx > ISO_MAX_LX || (comps != 1 && comps != 3)) return ERR_INVALID;
     if (!(max_error > 0.0 && max_error < 1.0)) return ERR_INVALID;
     const int n3 = lx * lx * lx, W = (n3 + 63) / 64;
@@ -372,7 +459,16 @@ int iso_compress(int lx, int comps, uint64_t n_elements, const double* field, do
             uint64_t* mk = masks + b * W;
             uint64_t lt, ld;
             int se, nf;
-            uint32_t kept = iso_select_block(lx, a, max_error, mk, &lt, &ld, &se, &nf);
+            uint32_t kept;
+            if (norm == 1) {
+                double umax = 0.0;
+                for (int j = 0; j < n3; ++j) umax = fmax(umax, fabs(u[j]));
+                kept = iso_select_block_linf(lx, Bm, a, umax, max_error, mk, &nf);
+                lt = ld = 0;
+                se = 0;
+            } else {
+                kept = iso_select_block(lx, a, max_error, mk, &lt, &ld, &se, &nf);
+            }
             if (nf) tbad[t] = 1;
             counts[b] = kept;
             tot += ldexp((double)lt, se);

@@ -69,12 +69,20 @@ uint32_t iso_select_block(int lx, const double* a, double max_error, uint64_t* m
 uint32_t iso_select_block_perturbed(int lx, const double* a, double max_error, double rel,
                                     uint64_t* mask);
 
+/* RelativeLInf rule: Bm = synthesis matrix [i*lx+k], umax = max|u| of the
+ * block's nodal values.  Returns the kept count and writes the mask. */
+uint32_t iso_select_block_linf(int lx, const double* Bm, const double* a, double umax, double max_error,
+                               uint64_t* mask, int* nonfinite);
+
 /* ---- whole fields ---- */
 uint64_t iso_stream_capacity(int lx, uint64_t nblocks);
 uint64_t iso_stream_header_bytes(int lx, uint64_t nblocks);  /* counts + masks */
 /* returns 0 or 1+ErrorCode (13 = ShapeMismatch, 21 = InvalidArgument) */
 int iso_compress(int lx, int comps, uint64_t n_elements, const double* field, double max_error,
                  uint8_t* stream, uint64_t cap, uint64_t* stream_bytes, iso_stats* st, int nthreads);
+/* norm: 0 = RelativeL2, 1 = RelativeLInf */
+int iso_compress_norm(int lx, int comps, uint64_t n_elements, const double* field, double max_error, int norm,
+                      uint8_t* stream, uint64_t cap, uint64_t* stream_bytes, iso_stats* st, int nthreads);
 int iso_decompress(int lx, int comps, uint64_t n_elements, const uint8_t* stream,
                    uint64_t stream_bytes, double* out, const double* original, iso_stats* st,
                    int nthreads);

@@ -63,6 +63,9 @@ def lib():
         L.iso_stream_header_bytes.argtypes = [i32, u64]
         L.iso_stream_header_bytes.restype = u64
         L.iso_compress.argtypes = [i32, i32, u64, P, f64, P, u64, P, P, i32]
+        L.iso_compress_norm.argtypes = [i32, i32, u64, P, f64, i32, P, u64, P, P, i32]
+        L.iso_select_block_linf.argtypes = [i32, P, P, f64, f64, P, P]
+        L.iso_select_block_linf.restype = ctypes.c_uint32
         L.iso_decompress.argtypes = [i32, i32, u64, P, u64, P, P, P, i32]
         L.iso_forward_field.argtypes = [i32, i32, u64, P, P, i32]
         L.iso_gen_tgv.argtypes = [i32, i32, i32, ctypes.c_uint32, ctypes.c_uint32, f64, P, i32]
@@ -136,17 +139,28 @@ def stream_header_bytes(lx, nblocks):
     return int(lib().iso_stream_header_bytes(lx, nblocks))
 
 
-def compress(field: np.ndarray, lx: int, comps: int, max_error: float, nthreads: int = 0):
-    """Returns (rc, stream bytes as np.uint8 array, Stats)."""
+def compress(field: np.ndarray, lx: int, comps: int, max_error: float, nthreads: int = 0, norm: int = 0):
+    """Returns (rc, stream bytes as np.uint8 array, Stats).  norm: 0 RelativeL2, 1 RelativeLInf."""
     field = np.ascontiguousarray(field, dtype=np.float64).reshape(-1)
     n_el = field.size // (lx ** 3 * comps)
     cap = stream_capacity(lx, n_el * comps)
     buf = np.zeros(cap, dtype=np.uint8)
     nb = ctypes.c_uint64()
     st = Stats()
-    rc = lib().iso_compress(lx, comps, n_el, _p(field), float(max_error), _p(buf), cap,
-                            ctypes.byref(nb), ctypes.byref(st), nthreads)
+    rc = lib().iso_compress_norm(lx, comps, n_el, _p(field), float(max_error), int(norm), _p(buf), cap,
+                                 ctypes.byref(nb), ctypes.byref(st), nthreads)
     return rc, buf[: nb.value].copy(), st
+
+
+def select_block_linf(lx: int, a: np.ndarray, umax: float, max_error: float):
+    """RelativeLInf rule on one block of coefficients: (kept, mask words)."""
+    _, B = matrices(lx)[:2]
+    B = np.ascontiguousarray(B, dtype=np.float64).reshape(-1)
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    mask = np.zeros((lx ** 3 + 63) // 64, dtype=np.uint64)
+    nf = ctypes.c_int()
+    kept = lib().iso_select_block_linf(lx, _p(B), _p(a), float(umax), float(max_error), _p(mask), ctypes.byref(nf))
+    return int(kept), mask, bool(nf.value)
 
 
 def decompress(stream: np.ndarray, lx: int, comps: int, n_elements: int, original=None,

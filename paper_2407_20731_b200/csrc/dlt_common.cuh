@@ -30,6 +30,7 @@ constexpr int kWTableSize = w_offset(kMaxLx + 1);
 __constant__ double c_ops[kOpTableSize];
 __constant__ double c_w[kWTableSize];
 __constant__ double c_x[kWTableSize];
+__constant__ double c_bm[kWTableSize];  // RelativeLInf: max_i |B[i][k]| per lx (w_offset layout)
 
 template <int LX>
 __device__ __forceinline__ double Fm(int k, int i) { return c_ops[op_offset(LX) + k * LX + i]; }
@@ -121,6 +122,7 @@ __host__ __device__ constexpr int ceil_log2(int v) {
 __host__ __device__ constexpr int energy_K(int lx) {
   return ((63 - ceil_log2(lx * lx * lx)) / 2) < 25 ? ((63 - ceil_log2(lx * lx * lx)) / 2) : 25;
 }
+__host__ __device__ constexpr int linf_K(int lx) { return 63 - ceil_log2(lx * lx * lx); }
 __device__ __forceinline__ uint64_t low52(double t) {
   return (uint64_t)__double_as_longlong(t) & 0x000FFFFFFFFFFFFFull;
 }
@@ -300,6 +302,116 @@ __device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const Src& s
     }
     const uint32_t d = g.min(dloc);
     if (d == 64) {  // everything undecided fits: discard it all
+      dsum += total;
+      tstar = khi;
+      icut = 0;
+      return;
+    }
+    const uint64_t ex = g.bcast(exloc, (int)(d / BPL));
+    R -= ex;
+    dsum += ex;
+    const uint64_t nlo = klo + ((uint64_t)d << shift);
+    const uint64_t nhi_full = nlo + ((1ull << shift) - 1);
+    const uint64_t nhi = nhi_full < khi ? nhi_full : khi;
+    uint64_t mn = ~0ull, mx = 0;
+    for (int p = g.rank; p < n; p += G) {
+      uint64_t k; uint32_t ix;
+      src(p, k, ix);
+      if (k >= nlo && k <= nhi) { mn = k < mn ? k : mn; mx = k > mx ? k : mx; }
+    }
+    klo = g.min(mn);
+    khi = g.max(mx);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// RelativeLInf truncation.
+// |u - u~|(x) <= sum_{j discarded} |a_j| * Bmax_j with Bmax_j = max|B(kx)| max|B(ky)|
+// max|B(kz)|.  Exact integer form (upper bounds for the discarded terms, a lower
+// bound for the budget):
+//   x_j = RU(|a_j| * RU(RU(bm_kx * bm_ky) * bm_kz)),   m = max_j x_j = f 2^s, f in [.5,1)
+//   k   = 53 - s,   w_j = x_j == 0 ? 0 : max(1, ceil(x_j 2^k))  (< 2^53)
+//   thr = floor(RD(eps * max|u|) 2^k)
+// and the discarded set is the longest prefix of the discard order (|a| asc, index
+// desc) with sum w <= thr; an all-zero block keeps nothing.
+// ---------------------------------------------------------------------------
+template <int LX>
+__device__ __forceinline__ double linf_bmax(int j) {
+  const int kx = j % LX, ky = (j / LX) % LX, kz = j / (LX * LX);
+  const int o = w_offset(LX);
+  return __dmul_ru(__dmul_ru(c_bm[o + kx], c_bm[o + ky]), c_bm[o + kz]);
+}
+__device__ __forceinline__ uint64_t linf_weight(double x, int k) {
+  if (x == 0.0) return 0;
+  const double c = ceil(scale2(x, k));
+  return c < 1.0 ? 1ull : (uint64_t)c;
+}
+
+// radix select over all n elements with per-element weights (general weights: the
+// tie group is resolved in index-descending order element by element)
+template <int G, class Src, class Wt>
+__device__ void radix_select_w(const LaneGroup<G>& g, const Src& src, const Wt& wt, int n, uint64_t R,
+                               unsigned long long* hist, uint64_t& tstar, uint32_t& icut, uint64_t& dsum) {
+  uint64_t klo = ~0ull, khi = 0;
+  for (int p = g.rank; p < n; p += G) {
+    uint64_t k; uint32_t ix;
+    src(p, k, ix);
+    klo = k < klo ? k : klo;
+    khi = k > khi ? k : khi;
+  }
+  klo = g.min(klo);
+  khi = g.max(khi);
+  dsum = 0;
+  for (;;) {
+    const uint64_t span = khi - klo;
+    if (span == 0) {
+      // tie group (key == klo): discard in index-descending order while the sum fits
+      uint32_t mine = 0xffffffffu;
+      uint64_t dloc = 0;
+      for (int p = g.rank; p < n; p += G) {
+        uint64_t k; uint32_t ip;
+        src(p, k, ip);
+        if (k != klo) continue;
+        uint64_t S = wt(k, ip);
+        const uint64_t own = S;
+        for (int q = 0; q < n; ++q) {
+          uint64_t kq; uint32_t iq;
+          src(q, kq, iq);
+          if (kq == klo && iq > ip) S += wt(kq, iq);
+        }
+        if (S <= R) { mine = ip < mine ? ip : mine; dloc += own; }
+      }
+      icut = (uint32_t)g.min((uint64_t)mine);
+      dsum += g.sum(dloc);
+      tstar = klo;
+      return;
+    }
+    const int bits = 64 - __clzll((long long)span);
+    const int shift = bits > 6 ? bits - 6 : 0;
+    for (int b = g.rank; b < 64; b += G) hist[b] = 0ull;
+    g.sync();
+    for (int p = g.rank; p < n; p += G) {
+      uint64_t k; uint32_t ix;
+      src(p, k, ix);
+      if (k >= klo && k <= khi) atomicAdd(&hist[(k - klo) >> shift], (unsigned long long)wt(k, ix));
+    }
+    g.sync();
+    constexpr int BPL = 64 / G;
+    uint64_t loc[BPL];
+    uint64_t run = 0;
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) { run += hist[g.rank * BPL + j]; loc[j] = run; }
+    const uint64_t base = g.exscan(run);
+    const uint64_t total = g.bcast(base + run, G - 1);
+    g.sync();
+    uint32_t dl = 64;
+    uint64_t exloc = 0;
+#pragma unroll
+    for (int j = BPL - 1; j >= 0; --j) {
+      if (base + loc[j] > R) { dl = g.rank * BPL + j; exloc = base + (j ? loc[j - 1] : 0); }
+    }
+    const uint32_t d = g.min(dl);
+    if (d == 64) {
       dsum += total;
       tstar = khi;
       icut = 0;

@@ -29,6 +29,8 @@ struct CompressArgs {
   uint64_t mask_off;  // byte offset of masks
   uint64_t val_off;   // byte offset of values
   uint64_t eps_q;     // floor(eps^2 * 2^64)
+  double eps;         // max_error (RelativeLInf budget)
+  int norm;           // ISF_NORM_RELATIVE_L2 (0) or ISF_NORM_RELATIVE_LINF (1; generic kernels)
   double* vslot;      // lx=8 fast path: per-tile value slots (2048 doubles per tile)
   Workspace ws;
 };
@@ -191,6 +193,60 @@ __device__ void select_generic(double* u, uint64_t eps_q, uint64_t* ckeys, uint1
   __syncwarp();
 }
 
+// RelativeLInf selection on warp 0 (dlt_common.cuh radix_select_w)
+template <int LX>
+__device__ void select_linf(const double* u, double umax, double eps, unsigned long long* hist, uint64_t* maskw,
+                            bool& nonfinite) {
+  constexpr int N3 = LX * LX * LX;
+  constexpr int NR = (N3 + 31) / 32;
+  const LaneGroup<32> g;
+  const int lane = g.rank;
+  for (int w = lane; w < 64; w += 32) maskw[w] = 0ull;
+  nonfinite = false;
+  uint64_t mb = 0, xm = 0;
+  for (int p = lane; p < N3; p += 32) {
+    const uint64_t b = abs_bits(u[p]);
+    mb = b > mb ? b : mb;
+    const uint64_t xb = (uint64_t)__double_as_longlong(__dmul_ru(fabs(u[p]), linf_bmax<LX>(p)));
+    xm = xb > xm ? xb : xm;
+  }
+  mb = g.max(mb);
+  xm = g.max(xm);
+  __syncwarp();
+  if (mb >= 0x7ff0000000000000ull || xm >= 0x7ff0000000000000ull) { nonfinite = true; return; }
+  if (xm == 0) return;  // all-zero block keeps nothing
+  int s;
+  {
+    const uint32_t hm = (uint32_t)(xm >> 32);
+    s = hm >= 0x00100000u ? (int)(hm >> 20) - 1022 : 64 - __clzll((long long)xm) - 1074;
+  }
+  const int k = linf_K(LX) - s;
+  auto wt = [&](uint64_t key, uint32_t ix) -> uint64_t {
+    return linf_weight(__dmul_ru(__longlong_as_double((long long)key), linf_bmax<LX>((int)ix)), k);
+  };
+  double tb = scale2(__dmul_rd(eps, umax), k);
+  tb = floor(tb);
+  const uint64_t thr = tb >= 9223372036854775808.0 ? (1ull << 63) : (uint64_t)tb;
+  uint64_t tot = 0;
+  for (int p = lane; p < N3; p += 32) tot += wt(abs_bits(u[p]), (uint32_t)p);
+  tot = g.sum(tot);
+  if (tot <= thr) return;  // the whole block fits in the budget
+  uint64_t tstar, dsum;
+  uint32_t icut;
+  radix_select_w<32>(g, SrcDense{u}, wt, N3, thr, hist, tstar, icut, dsum);
+  for (int r = 0; r < NR; ++r) {
+    const int p = r * 32 + lane;
+    bool kept = false;
+    if (p < N3) {
+      const uint64_t kk = abs_bits(u[p]);
+      kept = kk > tstar || (kk == tstar && (uint32_t)p < icut);
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, kept);
+    if (lane == 0) maskw[r >> 1] |= (uint64_t)b << (32 * (r & 1));
+  }
+  __syncwarp();
+}
+
 template <int LX>
 __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) {
   constexpr int N = LX, N2 = LX * LX, N3 = LX * LX * LX;
@@ -219,7 +275,18 @@ __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) 
     const uint64_t blk = tile;
     const uint64_t e = blk / A.comps, c = blk % A.comps;
     const double* src = A.field + e * (uint64_t)N3 * A.comps + c;
-    for (int p = tid; p < N3; p += kGenThreads) u[p] = src[(uint64_t)p * A.comps];
+    uint64_t um = 0;
+    for (int p = tid; p < N3; p += kGenThreads) {
+      const double x = src[(uint64_t)p * A.comps];
+      u[p] = x;
+      const uint64_t b = abs_bits(x);
+      um = b > um ? b : um;
+    }
+    if (A.norm) {  // RelativeLInf needs max|u| of the block
+      if (tid == 0) misc[3] = 0;
+      __syncthreads();
+      atomicMax(reinterpret_cast<unsigned long long*>(&misc[3]), (unsigned long long)um);
+    }
     __syncthreads();
     for (int l = tid; l < N2; l += kGenThreads) fwd_line_ptr<LX>(u + l, N2);                       // z
     __syncthreads();
@@ -231,7 +298,13 @@ __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) 
       uint64_t T, hd;
       int k;
       bool nf;
-      select_generic<LX>(u, A.eps_q, ckeys, cidx, hist, maskw, T, hd, k, nf);
+      if (A.norm) {
+        select_linf<LX>(u, __longlong_as_double((long long)misc[3]), A.eps, hist, maskw, nf);
+        T = hd = 0;
+        k = 0;
+      } else {
+        select_generic<LX>(u, A.eps_q, ckeys, cidx, hist, maskw, T, hd, k, nf);
+      }
       if (nf) {
         for (int w = lane; w < W; w += 32) maskw[w] = 0ull;
         if (lane == 0) atomicOr(A.ws.flags, kFlagNonFinite);

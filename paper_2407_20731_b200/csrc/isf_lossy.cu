@@ -54,12 +54,19 @@ int init_device_constants(int device) {
   std::lock_guard<std::mutex> lk(g_init_mu);
   if (device < 0 || device >= 64) return fail(ISF_E_INVALID_ARGUMENT, "device %d out of range", device);
   if (g_dev_init[device]) return 0;
-  static double ops[kOpTableSize], ws[kWTableSize], xs[kWTableSize];
+  static double ops[kOpTableSize], ws[kWTableSize], xs[kWTableSize], bms[kWTableSize];
   for (int lx = 2; lx <= kMaxLx; ++lx) {
     double x[kMaxLx], w[kMaxLx];
     build_operators(lx, ops + op_offset(lx), ops + op_offset(lx) + lx * lx, x, w);
     for (int i = 0; i < lx; ++i) { ws[w_offset(lx) + i] = w[i]; xs[w_offset(lx) + i] = x[i]; }
+    const double* Bm = ops + op_offset(lx) + lx * lx;  // B[i*lx + k]
+    for (int k = 0; k < lx; ++k) {
+      double m = 0.0;
+      for (int i = 0; i < lx; ++i) m = std::max(m, std::fabs(Bm[i * lx + k]));
+      bms[w_offset(lx) + k] = m;
+    }
   }
+  CUDA_TRY(cudaMemcpyToSymbol(c_bm, bms, sizeof bms));
   CUDA_TRY(cudaMemcpyToSymbol(c_ops, ops, sizeof ops));
   CUDA_TRY(cudaMemcpyToSymbol(c_w, ws, sizeof ws));
   CUDA_TRY(cudaMemcpyToSymbol(c_x, xs, sizeof xs));
@@ -341,8 +348,8 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   if (int rc = check_plan(p)) return rc;
   if (!(max_error > 0.0 && max_error < 1.0))
     return fail(ISF_E_INVALID_ARGUMENT, "LossyConfig: max_error must be in (0,1), got %g", max_error);
-  if (error_norm != ISF_NORM_RELATIVE_L2)
-    return fail(ISF_E_INVALID_ARGUMENT, "LossyConfig: only RelativeL2 truncation is implemented (norm=%d)", error_norm);
+  if (error_norm != ISF_NORM_RELATIVE_L2 && error_norm != ISF_NORM_RELATIVE_LINF)
+    return fail(ISF_E_INVALID_ARGUMENT, "LossyConfig: unknown error_norm %d", error_norm);
   if (n_elements == 0) return fail(ISF_E_INVALID_ARGUMENT, "empty field (0 elements)");
   if (!d_field || !d_stream || !d_stats) return fail(ISF_E_INVALID_ARGUMENT, "null device pointer");
   if (((uintptr_t)d_field & 15) || ((uintptr_t)d_stream & 15))
@@ -353,7 +360,7 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
                                   (unsigned long long)capacity, (unsigned long long)hdr);
   DeviceGuard dg(p->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  const bool fast = use_fast8(p);
+  const bool fast = use_fast8(p) && error_norm == ISF_NORM_RELATIVE_L2;  // RelativeLInf: generic kernels
   if (B >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
   const uint32_t ntiles = (uint32_t)B;  // generic: one tile per block; fast: one warp per block
   const uint32_t nchunks8 = (ntiles + kOffChunk - 1) / kOffChunk;
@@ -368,6 +375,8 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   a.mask_off = (4 * B + 15) & ~15ull;
   a.val_off = hdr;
   a.eps_q = eps_q_of(max_error);
+  a.eps = max_error;
+  a.norm = error_norm;
   a.vslot = nullptr;
   a.ws = Workspace{p->status, p->partials, p->counter, p->flags, next_epoch(p, s), ntiles, 0};
   const uint64_t* total_ptr = nullptr;

@@ -82,10 +82,10 @@ class LossyConfig:
         if not (0.0 < float(self.max_error) < 1.0):
             raise IsfError(ErrorCode.InvalidArgument,
                            f"LossyConfig: max_error must be in (0,1), got {self.max_error}")
-        if ErrorNorm(self.error_norm) != ErrorNorm.RelativeL2:
-            raise IsfError(ErrorCode.InvalidArgument,
-                           "LossyConfig: only RelativeL2 truncation is implemented "
-                           "(RelativeLInf is reported, not enforced)")
+        try:
+            ErrorNorm(self.error_norm)
+        except ValueError:
+            raise IsfError(ErrorCode.InvalidArgument, f"LossyConfig: unknown error_norm {self.error_norm}") from None
 
 
 @dataclass(frozen=True)

@@ -312,3 +312,33 @@ def test_decompress_bitexact(native, oracle, case):
     assert int(stats.view(torch.int64)[10].item()) == 0
     assert np.array_equal(got.view(np.uint64), ob.view(np.uint64))
     assert not np.any(got.view(np.uint64) == np.uint64(1 << 63))  # no -0 in the output
+
+
+@pytest.mark.parametrize("P,eps,kind", [(8, 1e-2, "tgv"), (8, 1e-4, "spectral"), (6, 1e-3, "spectral"),
+                                        (4, 1e-1, "spectral"), (12, 1e-3, "spectral"), (16, 1e-2, "spectral")])
+def test_linf_stream_bitexact_and_bound(native, oracle, P, eps, kind):
+    """RelativeLInf truncation: GPU stream byte-identical to the oracle,
+    reconstruction within eps * max|u| (global) through the error report."""
+    import paper_2407_20731_b200 as PK
+    E = 3 if P >= 12 else 4
+    n_el = E ** 3
+    u = oracle.gen_tgv(E, P, 0) if kind == "tgv" else oracle.gen_spectral(P, n_el)
+    f = _field(P, 1, n_el, u)
+    cfg = PK.LossyConfig(eps, PK.ErrorNorm.RelativeLInf)
+    blk = native.lossy_compress(f, cfg)
+    rc, ref, _ = oracle.compress(u, P, 1, eps, norm=1)
+    assert rc == 0
+    assert np.array_equal(blk.stream.cpu().numpy(), ref)
+    back, rep = native.decompress_with_error(blk, f.shape, f)
+    assert rep.rel_linf <= eps * (1 + 1e-9)
+
+
+def test_linf_vector_field(native, oracle):
+    import paper_2407_20731_b200 as PK
+    P, E = 8, 3
+    u = np.concatenate([oracle.gen_spectral(P, E ** 3, block0=b) for b in (0, 100, 200)])
+    v = u.reshape(3, -1, P ** 3).transpose(1, 2, 0).copy().reshape(-1)  # element, point, component
+    f = _field(P, 3, E ** 3, v)
+    blk = native.lossy_compress(f, PK.LossyConfig(1e-3, PK.ErrorNorm.RelativeLInf))
+    rc, ref, _ = oracle.compress(v, P, 3, 1e-3, norm=1)
+    assert rc == 0 and np.array_equal(blk.stream.cpu().numpy(), ref)
