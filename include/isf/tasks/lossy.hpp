@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <span>
 #include <string>
 #include <vector>
 
@@ -172,6 +173,94 @@ inline void lossy_compress_device(const double* d_field, std::uint64_t n_element
     cfg.validate();
     detail::check(isf_lossy_compress_async(detail::plan_for(P, comps), d_field, n_elements, cfg.max_error,
                                            static_cast<int>(cfg.error_norm), d_stream, capacity, d_stats, stream));
+}
+
+/// Device-resident kind-1 frame: compresses straight into
+/// d_frame + 48 and writes header, codec trailer and CRC-32 on the device
+/// (isf_lossy_frame_async).  d_frame holds stream capacity + ISF_FRAME_OVERHEAD
+/// bytes; the frame is d_stats->stream_bytes + ISF_FRAME_OVERHEAD bytes long.
+inline void lossy_compress_frame_device(const double* d_field, std::uint64_t n_elements, std::uint32_t E_ax,
+                                        std::uint32_t P, std::uint32_t comps, const LossyConfig& cfg,
+                                        void* d_frame, std::uint64_t frame_cap, isf_lossy_stats* d_stats,
+                                        std::uint64_t step_index, double sim_time, cudaStream_t stream) {
+    cfg.validate();
+    auto* plan = detail::plan_for(P, comps);
+    detail::check(isf_lossy_compress_async(plan, d_field, n_elements, cfg.max_error,
+                                           static_cast<int>(cfg.error_norm), static_cast<char*>(d_frame) + 48,
+                                           frame_cap - 48, d_stats, stream));
+    detail::check(isf_lossy_frame_async(plan, d_frame, frame_cap, d_stats, E_ax, step_index, sim_time, stream));
+}
+
+/// Synchronous prefix of the hybrid mode (SPEC.md run_hybrid):
+/// the device frame copied to an owned host frame for StageWriter::write_frame
+/// (staging.hpp:59-60).  Only the compressed frame crosses PCIe.
+inline Bytes lossy_compress_frame(const double* d_field, std::uint64_t n_elements, std::uint32_t E_ax,
+                                  std::uint32_t P, std::uint32_t comps, const LossyConfig& cfg,
+                                  std::uint64_t step_index = 0, double sim_time = 0.0,
+                                  cudaStream_t stream = nullptr) {
+    struct Bufs {
+        void* frame = nullptr;
+        std::uint64_t cap = 0;
+        isf_lossy_stats* stats = nullptr;
+        ~Bufs() { cudaFree(frame); cudaFree(stats); }
+    };
+    thread_local Bufs b;
+    const std::uint64_t cap = isf_lossy_stream_capacity(P, comps, n_elements) + ISF_FRAME_OVERHEAD;
+    if (cap > b.cap) {
+        cudaFree(b.frame);
+        b.frame = nullptr;
+        if (cudaMalloc(&b.frame, cap) != cudaSuccess) throw Error(ErrorCode::TaskFailed, "cudaMalloc frame");
+        b.cap = cap;
+    }
+    if (!b.stats && cudaMalloc(&b.stats, sizeof(isf_lossy_stats)) != cudaSuccess)
+        throw Error(ErrorCode::TaskFailed, "cudaMalloc stats");
+    lossy_compress_frame_device(d_field, n_elements, E_ax, P, comps, cfg, b.frame, b.cap, b.stats, step_index,
+                                sim_time, stream);
+    isf_lossy_stats st{};
+    if (cudaMemcpyAsync(&st, b.stats, sizeof st, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess)
+        throw Error(ErrorCode::TaskFailed, "frame statistics copy failed");
+    if (st.status & ISF_STATUS_NONFINITE) throw Error(ErrorCode::InvalidArgument, "Field: non-finite value");
+    if (st.status) throw Error(ErrorCode::SerializationFailed, "frame assembly failed");
+    Bytes out(st.stream_bytes + ISF_FRAME_OVERHEAD);
+    if (cudaMemcpy(out.data(), b.frame, out.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw Error(ErrorCode::TaskFailed, "frame copy failed");
+    return out;
+}
+
+/// Inverse of CompressedBlock::payload(): a block from a kind-1 payload (the
+/// stream is everything before the SPEC.md:282 codec trailer).
+inline CompressedBlock block_from_payload(std::span<const std::byte> payload, const FrameHeader& h,
+                                          std::uint64_t n_elements) {
+    if (payload.size() < 10) throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its trailer");
+    CompressedBlock b;
+    b.elements_per_axis = h.elements_per_axis;
+    b.points_per_element_axis = h.points_per_element_axis;
+    b.components = h.components;
+    b.n_elements = n_elements;
+    // the stream length follows from its own counts: header + 8 * sum(counts)
+    const std::uint64_t B = n_elements * h.components;
+    const std::uint64_t hdr = isf_lossy_stream_header_bytes(h.points_per_element_axis, h.components, n_elements);
+    if (payload.size() < hdr + 10) throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its header");
+    std::uint64_t total = 0;
+    for (std::uint64_t i = 0; i < B; ++i) {
+        std::uint32_t c = 0;
+        std::memcpy(&c, payload.data() + 4 * i, 4);
+        total += c;
+    }
+    const std::size_t sb = hdr + 8 * total;
+    if (payload.size() < sb + 10) throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its stream");
+    std::uint64_t coded = 0;
+    std::memcpy(&coded, payload.data() + sb + 2, 8);
+    if (sb + 10 + coded != payload.size()) throw Error(ErrorCode::LengthMismatch, "kind-1 payload length mismatch");
+    b.stream.assign(payload.begin(), payload.begin() + sb);
+    b.lossless_codec = std::uint16_t(std::to_integer<std::uint8_t>(payload[sb])) |
+                       std::uint16_t(std::uint16_t(std::to_integer<std::uint8_t>(payload[sb + 1])) << 8);
+    b.coded_bytes.assign(payload.begin() + sb + 10, payload.begin() + sb + 10 + coded);
+    b.report = CompressionReport::from_sizes(n_elements * h.points_per_element_axis * h.points_per_element_axis *
+                                                 h.points_per_element_axis * h.components * 8,
+                                             b.stream.size());
+    return b;
 }
 
 inline void lossy_decompress_device(const void* d_stream, std::uint64_t stream_bytes, std::uint64_t n_elements,
