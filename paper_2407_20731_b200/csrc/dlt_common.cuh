@@ -485,6 +485,78 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------------------
+// Tensor memory (tcgen05) as a second on-chip buffer beside shared memory.
+// The lx = 8 kernels use it for register re-layouts and to park coefficients: its
+// datapath is separate from the shared-memory banks (128 B/clk/SM, the limit of the
+// smem-only design) and a 4 KiB store + 16x256b re-read runs at ~358 B/clk/SM
+// (tools/probe/tmem_bw.cu).  Thread <-> (lane, column) maps measured by
+// tools/probe/tmem_probe.cu:
+//   32x32b : thread t <-> lane t, register i <-> column i
+//   16x256b.xN at lane L : register 4j + 2h + e <-> lane L + 8h + t/4,
+//                          column 2(t%4) + e + 8j
+// A warp may only touch lanes 32 (warp % 4) .. + 31.
+// ---------------------------------------------------------------------------
+template <uint32_t NCOLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t* smem_dst) {  // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)), "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <uint32_t NCOLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {  // whole warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+#define ISF_R8(b) "r"(r[b]), "r"(r[b + 1]), "r"(r[b + 2]), "r"(r[b + 3]), "r"(r[b + 4]), "r"(r[b + 5]), "r"(r[b + 6]), "r"(r[b + 7])
+#define ISF_W8(b) "=r"(r[b]), "=r"(r[b + 1]), "=r"(r[b + 2]), "=r"(r[b + 3]), "=r"(r[b + 4]), "=r"(r[b + 5]), "=r"(r[b + 6]), "=r"(r[b + 7])
+// 32x32b.x32: thread t's 32 words -> lane t, columns 0..31 (16 doubles as lo/hi pairs)
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t ta, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+      ISF_R8(0), ISF_R8(8), ISF_R8(16), ISF_R8(24)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t ta, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : ISF_W8(0), ISF_W8(8), ISF_W8(16), ISF_W8(24)
+      : "r"(ta)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t ta, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : ISF_W8(0), ISF_W8(8)
+      : "r"(ta)
+      : "memory");
+}
+#undef ISF_R8
+#undef ISF_W8
+// 16 doubles parked at columns 0..31 of the thread's lane -> registers (waits)
+__device__ __forceinline__ void tmem_load16(uint32_t ta, double (&c)[16]) {
+  uint32_t r[32];
+  tmem_ld_32x32b_x32(ta, r);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) c[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+__device__ __forceinline__ void tmem_store16(uint32_t ta, const double (&c)[16]) {
+  uint32_t r[32];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    r[2 * i] = (uint32_t)__double2loint(c[i]);
+    r[2 * i + 1] = (uint32_t)__double2hiint(c[i]);
+  }
+  tmem_st_32x32b_x32(ta, r);
+}
+
+// ---------------------------------------------------------------------------
 // Decoupled look-back over warp tiles (single-pass variable-length output).
 // status word: [63:40] epoch, [39:38] flag (1 aggregate, 2 inclusive), [37:0] value
 // ---------------------------------------------------------------------------

@@ -28,7 +28,11 @@ namespace dev {
 #endif
 constexpr int kC8Warps = ISF_C8_WARPS;  // compress warps per CTA
 constexpr int kD8Warps = ISF_D8_WARPS;  // decompress warps per CTA
-constexpr int kF8Stages = 2;   // TMA ring depth per warp
+constexpr int kF8Stages = 2;   // TMA ring depth per warp (decompress)
+#ifndef ISF_C8_STAGES
+#define ISF_C8_STAGES 2
+#endif
+constexpr int kC8Stages = ISF_C8_STAGES;  // TMA ring depth per warp (compress)
 
 // 16-byte chunk c (0..31) of plane kz (512 B)
 __device__ __forceinline__ int swz(int kz, int c) { return c ^ (((c >> 3) & 3) | ((kz & 1) << 2)); }
@@ -84,11 +88,13 @@ __device__ __forceinline__ uint32_t warp_exscan_u32(uint32_t v, int lane) {
 // (same algorithm as radix_select in dlt_common.cuh, elements in registers).
 // out = {t*, icut, discarded hi-sum}.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void radix_select16(const double* vin, int lane, uint64_t R, double f, double pre,
+__device__ __noinline__ void radix_select16(uint32_t tpark, int lane, uint64_t R, double f, double pre,
                                             unsigned long long* hist, uint64_t* out) {
-  double v[16];  // vin: [pair][lane] double2 layout; pre: exact tiny-block pre-scale (else 1)
+  double v[16];  // the parked coefficients (TMEM); pre: exact tiny-block pre-scale (else 1)
+  tmem_wait_st();
+  tmem_load16(tpark, v);
 #pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = __dmul_rn(vin[((r >> 1) * 32 + lane) * 2 + (r & 1)], pre);
+  for (int r = 0; r < 16; ++r) v[r] = __dmul_rn(v[r], pre);
   uint64_t klo = ~0ull, khi = 0;
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
@@ -206,15 +212,11 @@ struct Sel16 {
 };
 
 // v[r] = coefficient 16*lane + r of the warp's block (consumed: only pass 0/1 read
-// it); coef2 = the same coefficients parked in shared memory as [pair][lane] double2
-// (read by the one-move and general paths and by the encoder).
+// it); tpark = the same coefficients parked in tensor memory (32x32b, lane = thread,
+// columns 2r, 2r+1), re-read by the one-move and general paths and by the encoder.
 __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t eps_q, unsigned long long* hist,
-                                          const double2* coef2) {
+                                          uint32_t tpark) {
   Sel16 s{0u, 0ull, 0ull, 0, false};
-  auto coef = [&](int r) -> double {
-    const double2 t = coef2[(r >> 1) * 32 + lane];
-    return (r & 1) ? t.y : t.x;
-  };
 #ifdef ISF_OPT_DMAX
   // max |a| by fp64 max (NaN-ignoring); a non-finite input makes every coefficient of
   // the lx=8 block non-finite (no zero in F), so the lane maximum is Inf or NaN then
@@ -333,9 +335,12 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   } else {
     uint64_t mk = 0;
     int mi = 16;
+    double c16[16];
+    tmem_wait_st();
+    tmem_load16(tpark, c16);
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const uint64_t kk = ((cm >> r) & 1u) ? abs_bits(coef(r)) + 1ull : 0ull;  // +1: zeros count
+      const uint64_t kk = ((cm >> r) & 1u) ? abs_bits(c16[r]) + 1ull : 0ull;  // +1: zeros count
       if (kk > mk) { mk = kk; mi = r; }
     }
     const uint64_t gmk = warp_max_u64(mk);
@@ -348,13 +353,15 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
     return s;
   }
   uint64_t res[3];
-  radix_select16(reinterpret_cast<const double*>(coef2), lane, thr, f, pre, hist, res);
+  radix_select16(tpark, lane, thr, f, pre, hist, res);
   const uint64_t tstar = res[0];
   const uint32_t icut = (uint32_t)res[1];
   uint32_t mk2 = 0;
+  double c16[16];
+  tmem_load16(tpark, c16);
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    const uint64_t kk = abs_bits(__dmul_rn(coef(r), pre));
+    const uint64_t kk = abs_bits(__dmul_rn(c16[r], pre));
     const uint32_t j = (uint32_t)(16 * lane + r);
     if (kk > tstar || (kk == tstar && j < icut)) mk2 |= 1u << r;
   }
@@ -364,27 +371,38 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
 }
 
 // --------------------------- compress ---------------------------------------
-constexpr int kC8WarpBytes = kF8Stages * 4096 + 768 + 128;  // stages | hist (3 x 64 u32) | mbarriers
+constexpr int kC8WarpBytes = kC8Stages * 4096 + 768 + 128;  // stages | hist (3 x 64 u32) | mbarriers
 constexpr int kC8Smem = kC8Warps * kC8WarpBytes;
+// TMEM columns per warp: [0, 32) y->x re-layout buffer, [32, 64) parked coefficients;
+// the four warps of a lane quadrant (warp % 4) sit side by side.
+constexpr uint32_t kC8TmemCols = 64u * (kC8Warps / 4);
+static_assert(kC8Warps % 4 == 0 && kC8TmemCols <= 512, "TMEM budget");
 
 __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A) {
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t s_tmem;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned char* wbase = smem + warp * kC8WarpBytes;
-  unsigned long long* hist = reinterpret_cast<unsigned long long*>(wbase + kF8Stages * 4096);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kF8Stages * 4096 + 768);
-  const int kzp = lane >> 2, qp = lane & 3;  // y-line / x-line roles
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(wbase + kC8Stages * 4096);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kC8Stages * 4096 + 768);
+  const int kzy = lane & 7, qy = lane >> 3;  // y-line role: plane kz, x pair q
   uint32_t* counts = reinterpret_cast<uint32_t*>(A.stream);
   uint16_t* masks16 = reinterpret_cast<uint16_t*>(A.stream + A.mask_off);
   const uint64_t W = (uint64_t)gridDim.x * kC8Warps;
   const uint64_t gw = (uint64_t)blockIdx.x * kC8Warps + warp;
   const uint64_t B = A.nblocks;
+  if (warp == 0) tmem_alloc<kC8TmemCols>(&s_tmem);
   if (lane == 0) {
 #pragma unroll
-    for (int s = 0; s < kF8Stages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kC8Stages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
   }
-  __syncwarp();
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = s_tmem;
+  const uint32_t tx = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (uint32_t)(warp >> 2);
+  const uint32_t tpark = tx + 32u;
   auto issue = [&](uint64_t blk, int st) {
     if (lane == 0 && blk < B) {
       mbar_arrive_tx(&bars[st], 4096u);
@@ -392,7 +410,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     }
   };
 #pragma unroll
-  for (int s = 0; s < kF8Stages; ++s) issue(gw + s * W, s);
+  for (int s = 0; s < kC8Stages; ++s) issue(gw + s * W, s);
   double tot_acc = 0.0, disc_acc = 0.0;
   int st = 0;
   uint32_t ph = 0;
@@ -401,6 +419,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     mbar_wait(&bars[st], (ph >> st) & 1u);
     ph ^= 1u << st;
     double v[16];
+    // z-lines: lane = (y = l/4, q = l%4) holds x = 2q, 2q+1 of row y for all z
 #pragma unroll
     for (int z = 0; z < 8; ++z) {
       const double2 t = sb[z * 32 + lane];
@@ -411,45 +430,63 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
 #ifndef ISF_EXP_NOXFORM
     lines<8, 2, 0, 1, 2, false>(v);  // z sweep
 #endif
+    // z -> y re-layout through the stage (in place): 16-B chunk c of plane kz at
+    // kz * 32 + (c ^ kz), conflict free for both access patterns
 #pragma unroll
-    for (int kz = 0; kz < 8; ++kz) sb[kz * 32 + swz(kz, lane)] = make_double2(v[2 * kz], v[2 * kz + 1]);
+    for (int kz = 0; kz < 8; ++kz) sb[kz * 32 + (lane ^ kz)] = make_double2(v[2 * kz], v[2 * kz + 1]);
     __syncwarp();
+    // y-lines: lane = (q = l/8, kz = l%8) holds x = 2q, 2q+1 for all y at plane kz
 #pragma unroll
     for (int y = 0; y < 8; ++y) {
-      const double2 t = sb[kzp * 32 + swz(kzp, y * 4 + qp)];
+      const double2 t = sb[kzy * 32 + ((4 * y + qy) ^ kzy)];
       v[2 * y] = t.x;
       v[2 * y + 1] = t.y;
     }
+    fence_proxy_async();
     __syncwarp();
+    issue(blk + kC8Stages * W, st);  // the stage is free: refill it now
+    st = (st + 1 == kC8Stages) ? 0 : st + 1;
 #ifndef ISF_EXP_NOXFORM
-    lines<8, 2, 0, 1, 2, false>(v);  // y sweep
+    lines<8, 2, 0, 1, 2, false>(v);  // y sweep: v[2 ky + x0]
 #endif
+    // y -> x re-layout through TMEM: store 32x32b with column pair
+    // c = (ky0, x0, ky2, ky1) [bits 3..0], re-read 16x256b at lanes 0 and 16.  Reader
+    // lane u gets (source lane bits 2..0, c bits 1..0) = (kz, ky2 ky1): the x-line
+    // role; its double (g, j, h) of instruction g, rep j, half h holds
+    // x2 = g, x1 = h, ky0 = j1, x0 = j0.
+    {
+      uint32_t r[32];
 #pragma unroll
-    for (int ky = 0; ky < 8; ++ky) sb[kzp * 32 + swz(kzp, ky * 4 + qp)] = make_double2(v[2 * ky], v[2 * ky + 1]);
-    __syncwarp();
-#pragma unroll
-    for (int kyi = 0; kyi < 2; ++kyi)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double2 t = sb[kzp * 32 + swz(kzp, (2 * qp + kyi) * 4 + q)];
-        v[kyi * 8 + 2 * q] = t.x;
-        v[kyi * 8 + 2 * q + 1] = t.y;
+      for (int c = 0; c < 16; ++c) {
+        const int ky = ((c >> 1) & 1) * 4 + (c & 1) * 2 + (c >> 3), x0 = (c >> 2) & 1;
+        r[2 * c] = (uint32_t)__double2loint(v[2 * ky + x0]);
+        r[2 * c + 1] = (uint32_t)__double2hiint(v[2 * ky + x0]);
       }
-    __syncwarp();
+      tmem_st_32x32b_x32(tx, r);
+      tmem_wait_st();
+      uint32_t a0[16], a1[16];
+      tmem_ld_16x256b_x4(tx, a0);
+      tmem_ld_16x256b_x4(tx + (16u << 16), a1);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int dst = (j >> 1) * 8 + h * 2 + (j & 1);  // kyi * 8 + x, x = 4 g + 2 h + j0
+          v[dst] = __hiloint2double((int)a0[4 * j + 2 * h + 1], (int)a0[4 * j + 2 * h]);
+          v[dst + 4] = __hiloint2double((int)a1[4 * j + 2 * h + 1], (int)a1[4 * j + 2 * h]);
+        }
+    }
 #ifndef ISF_EXP_NOXFORM
     lines<8, 1, 0, 8, 2, false>(v);  // x sweep: v[r] = coefficient 16*lane + r
 #endif
-    // park the coefficients in the stage as [pair][lane] double2 (conflict free);
-    // the registers are then free for the selection
-    double2* coef2 = reinterpret_cast<double2*>(sb);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) coef2[r * 32 + lane] = make_double2(v[2 * r], v[2 * r + 1]);
-    __syncwarp();
+    // park the coefficients in TMEM; the registers are then free for the selection
+    tmem_store16(tpark, v);
 #ifdef ISF_EXP_NOSEL
     Sel16 sel{0u, 1ull, 0ull, 0, false};
     if (__double_as_longlong(v[0]) == 0x1234) sel.mask = 1;
 #else
-    const Sel16 sel = select16(v, lane, A.eps_q, hist, coef2);
+    const Sel16 sel = select16(v, lane, A.eps_q, hist, tpark);
 #endif
     if (sel.nonfinite && lane == 0) atomicOr(A.ws.flags, kFlagNonFinite);
     const uint32_t mask = sel.nonfinite ? 0u : sel.mask;
@@ -458,20 +495,15 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     if (lane == 0) counts[blk] = kept;  // the 16-B pad is zeroed by block_offsets8_kernel
     masks16[blk * 32 + lane] = (uint16_t)mask;
     // kept values from the parked copy, written by their owner lane in index order
-    {
-      const double* cf = reinterpret_cast<const double*>(coef2) + 2 * lane;
+    tmem_wait_st();
+    if (kept) {
+      double c16[16];
+      tmem_load16(tpark, c16);
       double* dst = A.vslot + blk * 512 + off;
-      uint32_t m = mask;
-      while (m) {
-        const int r = __ffs(m) - 1;
-        m &= m - 1;
-        *dst++ = cf[(r >> 1) * 64 + (r & 1)];
-      }
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if ((mask >> r) & 1u) *dst++ = c16[r];
     }
-    fence_proxy_async();
-    __syncwarp();
-    issue(blk + kF8Stages * W, st);  // refill this stage
-    st = (st + 1 == kF8Stages) ? 0 : st + 1;
     if (!sel.nonfinite && sel.T) {
       tot_acc += scale2((double)sel.T, -2 * sel.k);
       disc_acc += scale2((double)sel.hdisc, -2 * sel.k);
@@ -481,6 +513,9 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     A.ws.partials[gw * 4 + 0] = tot_acc;
     A.ws.partials[gw * 4 + 1] = disc_acc;
   }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<kC8TmemCols>(tbase);
 }
 
 // --------------------------- block offsets / compact passes -----------------
