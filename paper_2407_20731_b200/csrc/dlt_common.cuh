@@ -536,6 +536,9 @@ __device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t ta, uint32_t (&r)[16
       : "r"(ta)
       : "memory");
 }
+__device__ __forceinline__ void tmem_ld_32x32b_x2(uint32_t ta, uint32_t& lo, uint32_t& hi) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(ta) : "memory");
+}
 #undef ISF_R8
 #undef ISF_W8
 // 16 doubles parked at columns 0..31 of the thread's lane -> registers (waits)

@@ -371,7 +371,10 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
 }
 
 // --------------------------- compress ---------------------------------------
-constexpr int kC8WarpBytes = kC8Stages * 4096 + 768 + 128;  // stages | hist (3 x 64 u32) | mbarriers
+// stage: the block's 4 KiB as loaded by the TMA engine, re-used in place for the z -> y
+// re-layout with a plane stride of 33 16-B chunks (528 B; conflict free both ways)
+constexpr int kC8Stage = 33 * 8 * 16;
+constexpr int kC8WarpBytes = kC8Stages * kC8Stage + 768 + 128;  // stages | hist (3 x 64 u32) | mbarriers
 constexpr int kC8Smem = kC8Warps * kC8WarpBytes;
 // TMEM columns per warp: [0, 32) y->x re-layout buffer, [32, 64) parked coefficients;
 // the four warps of a lane quadrant (warp % 4) sit side by side.
@@ -383,9 +386,9 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   __shared__ uint32_t s_tmem;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned char* wbase = smem + warp * kC8WarpBytes;
-  unsigned long long* hist = reinterpret_cast<unsigned long long*>(wbase + kC8Stages * 4096);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kC8Stages * 4096 + 768);
-  const int kzy = lane & 7, qy = lane >> 3;  // y-line role: plane kz, x pair q
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(wbase + kC8Stages * kC8Stage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kC8Stages * kC8Stage + 768);
+  const int yoff = (lane & 7) * 33 + (lane >> 3);  // y-line role (plane kz = l%8, x pair q = l/8)
   uint32_t* counts = reinterpret_cast<uint32_t*>(A.stream);
   uint16_t* masks16 = reinterpret_cast<uint16_t*>(A.stream + A.mask_off);
   const uint64_t W = (uint64_t)gridDim.x * kC8Warps;
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   auto issue = [&](uint64_t blk, int st) {
     if (lane == 0 && blk < B) {
       mbar_arrive_tx(&bars[st], 4096u);
-      bulk_g2s_evict_first(wbase + st * 4096, A.field + blk * 512, 4096u, &bars[st]);
+      bulk_g2s_evict_first(wbase + st * kC8Stage, A.field + blk * 512, 4096u, &bars[st]);
     }
   };
 #pragma unroll
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   int st = 0;
   uint32_t ph = 0;
   for (uint64_t blk = gw; blk < B; blk += W) {
-    double2* sb = reinterpret_cast<double2*>(wbase + st * 4096);
+    double2* sb = reinterpret_cast<double2*>(wbase + st * kC8Stage);
     mbar_wait(&bars[st], (ph >> st) & 1u);
     ph ^= 1u << st;
     double v[16];
@@ -431,14 +434,14 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     lines<8, 2, 0, 1, 2, false>(v);  // z sweep
 #endif
     // z -> y re-layout through the stage (in place): 16-B chunk c of plane kz at
-    // kz * 32 + (c ^ kz), conflict free for both access patterns
+    // kz * 33 + c (all reads of the stage are done)
 #pragma unroll
-    for (int kz = 0; kz < 8; ++kz) sb[kz * 32 + (lane ^ kz)] = make_double2(v[2 * kz], v[2 * kz + 1]);
+    for (int kz = 0; kz < 8; ++kz) sb[kz * 33 + lane] = make_double2(v[2 * kz], v[2 * kz + 1]);
     __syncwarp();
     // y-lines: lane = (q = l/8, kz = l%8) holds x = 2q, 2q+1 for all y at plane kz
 #pragma unroll
     for (int y = 0; y < 8; ++y) {
-      const double2 t = sb[kzy * 32 + ((4 * y + qy) ^ kzy)];
+      const double2 t = sb[yoff + 4 * y];
       v[2 * y] = t.x;
       v[2 * y + 1] = t.y;
     }
@@ -494,15 +497,20 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     const uint32_t off = warp_exscan_small((uint32_t)__popc(mask), lane, kept);
     if (lane == 0) counts[blk] = kept;  // the 16-B pad is zeroed by block_offsets8_kernel
     masks16[blk * 32 + lane] = (uint16_t)mask;
-    // kept values from the parked copy, written by their owner lane in index order
-    tmem_wait_st();
-    if (kept) {
-      double c16[16];
-      tmem_load16(tpark, c16);
+    // kept values from the parked copy, written by their owner lane in index order:
+    // one TMEM column pair per register slot r occupied in any lane
+    uint32_t um = __reduce_or_sync(0xffffffffu, mask);
+    if (um) {
+      tmem_wait_st();
       double* dst = A.vslot + blk * 512 + off;
-#pragma unroll
-      for (int r = 0; r < 16; ++r)
-        if ((mask >> r) & 1u) *dst++ = c16[r];
+      do {
+        const int r = __ffs(um) - 1;
+        um &= um - 1;
+        uint32_t lo, hi;
+        tmem_ld_32x32b_x2(tpark + 2u * (uint32_t)r, lo, hi);
+        tmem_wait_ld();
+        if ((mask >> r) & 1u) *dst++ = __hiloint2double((int)hi, (int)lo);
+      } while (um);
     }
     if (!sel.nonfinite && sel.T) {
       tot_acc += scale2((double)sel.T, -2 * sel.k);

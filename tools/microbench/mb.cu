@@ -93,6 +93,59 @@ __global__ void k_bulkstore(unsigned char* __restrict__ b, size_t nbytes) {
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+
+// TMA bulk-load read: each warp streams 4 KiB blocks (round robin) through an S-stage ring
+__device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t ph) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("{\n.reg .pred p;\nW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W;\n}" ::"r"(sa), "r"(ph) : "memory");
+}
+template <int S>
+__global__ void k_bulkread(const unsigned char* __restrict__ a, size_t nblk, double* out) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  unsigned char* mine = sm + warp * (S * 4096 + 64);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(mine + S * 4096);
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) { unsigned sa = (unsigned)__cvta_generic_to_shared(&bars[s]); asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa)); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const size_t W = (size_t)gridDim.x * nw, gw = (size_t)blockIdx.x * nw + warp;
+  auto issue = [&](size_t blk, int st) {
+    if (lane == 0 && blk < nblk) {
+      unsigned sb = (unsigned)__cvta_generic_to_shared(&bars[st]);
+      unsigned sd = (unsigned)__cvta_generic_to_shared(mine + st * 4096);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 4096;" ::"r"(sb) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 4096, [%2];" ::"r"(sd), "l"(a + blk * 4096), "r"(sb) : "memory");
+    }
+  };
+  for (int s = 0; s < S; ++s) issue(gw + s * W, s);
+  double acc = 0; int st = 0; uint32_t ph = 0;
+  for (size_t blk = gw; blk < nblk; blk += W) {
+    mb_wait(&bars[st], (ph >> st) & 1u); ph ^= 1u << st;
+    const double2* p = reinterpret_cast<const double2*>(mine + st * 4096);
+#pragma unroll
+    for (int z = 0; z < 8; ++z) { double2 v = p[z * 32 + lane]; acc += v.x; }
+    __syncwarp();
+    issue(blk + S * W, st);
+    st = st + 1 == S ? 0 : st + 1;
+  }
+  if (acc == 1.2345) out[0] = acc;
+}
+// LDG read with a warp per 4 KiB block (8 x 128-bit loads per lane, all issued before use)
+__global__ void k_warpread(const double2* __restrict__ a, size_t nblk, double* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const size_t W = (size_t)gridDim.x * nw, gw = (size_t)blockIdx.x * nw + warp;
+  double acc = 0;
+  for (size_t blk = gw; blk < nblk; blk += W) {
+    double2 v[8];
+#pragma unroll
+    for (int z = 0; z < 8; ++z) v[z] = __ldcs(a + blk * 256 + z * 32 + lane);
+#pragma unroll
+    for (int z = 0; z < 8; ++z) acc += v[z].x;
+  }
+  if (acc == 1.2345) out[0] = acc;
+}
 int main(int argc, char** argv) {
   int dev = 0; cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, dev));
   int sms = p.multiProcessorCount;
@@ -149,5 +202,20 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&ms, e0, e1);
     printf("bulkstore grid=%d*SM: %.1f GB/s\n", bs > 2 ? 2 : bs, 5.0 * n * 16 / (ms * 1e6));
   }
+  {
+    const size_t nblk = n * 16 / 4096;
+    auto run = [&](const char* name, auto launch) {
+      launch();
+      cudaEventRecord(e0); for (int r = 0; r < 5; r++) launch(); cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("%s: %.1f GB/s\n", name, 5.0 * n * 16 / (ms * 1e6));
+      return 0;
+    };
+#define BR(S, NW) { const int sm_ = NW * (S * 4096 + 64); cudaFuncSetAttribute(k_bulkread<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_); \
+      char nm[64]; snprintf(nm, 64, "bulkread S=%d warps=%d", S, NW); run(nm, [&] { k_bulkread<S><<<sms, NW * 32, sm_>>>((const unsigned char*)a, nblk, dout); }); }
+    BR(2, 16) BR(3, 16) BR(2, 8) BR(4, 8) BR(6, 8) BR(4, 12) BR(1, 32) BR(2, 24)
+    for (int nw : {8, 16, 32}) for (int bs : {1, 2, 4}) { char nm[64]; snprintf(nm, 64, "warpread warps=%d grid=%d*SM", nw, bs); run(nm, [&] { k_warpread<<<sms * bs, nw * 32>>>(a, nblk, dout); }); }
+  }
+  
   return 0;
 }
