@@ -203,6 +203,12 @@ __device__ __noinline__ void radix_select16(uint32_t tpark, int lane, uint64_t R
   }
 }
 
+#ifdef ISF_PATHSTATS
+__device__ unsigned long long g_pathstats[16];
+#define ISF_PATH(P_) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_pathstats[P_], 1ull); } while (0)
+#else
+#define ISF_PATH(P_) do {} while (0)
+#endif
 struct Sel16 {
   uint32_t mask;   // kept bits of this lane's 16 coefficients
   uint64_t T;      // block total of lo energies
@@ -277,14 +283,7 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   const double tthr = 4503599627370496.0 + (double)(thr < (1ull << 51) ? thr : (1ull << 51));
   uint32_t mH = 0;
   uint64_t h0 = 0, h1s = 0;
-#ifdef ISF_OPT_FUSEMAX
-  double tmd = 0.0;  // largest t outside H (for the one-move path)
-#pragma unroll
-  for (int r = 0; r < 16; r += 2) {
-    if (t[r] >= tthr) { mH |= 1u << r; h0 += (uint64_t)__double_as_longlong(t[r]); } else tmd = fmax(tmd, t[r]);
-    if (t[r + 1] >= tthr) { mH |= 1u << (r + 1); h1s += (uint64_t)__double_as_longlong(t[r + 1]); } else tmd = fmax(tmd, t[r + 1]);
-  }
-#elif defined(ISF_OPT_HINT)
+#if defined(ISF_OPT_HINT)
   // integer classification (keeps the FP64 pipe free): t >= tthr <=> bits(t) >= bits(tthr)
   const uint64_t tthr_b = C52 + (thr < (1ull << 51) ? thr : (1ull << 51));
 #pragma unroll
@@ -305,52 +304,60 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   const uint32_t NH = __reduce_add_sync(0xffffffffu, nH);
   const uint64_t SN = T - SH + (512u - NH);                  // sum of hi over the rest
   if (SN <= thr) {
+    ISF_PATH(1);
     s.mask = mH;
     s.hdisc = SN;
     return s;
   }
-  // One-move path: the last element of the non-kept prefix (largest |a|, smallest
-  // index among ties) joins the kept set if that suffices.
+  // Few-move path: the last element of the non-kept prefix (largest |a|, smallest
+  // index among ties) joins the kept set, repeated until the rest fits under thr
+  // (the next elements of the pinned order, so the result is the exact rule's).
   // t is monotone in |a|: the largest t among the non-kept gives the candidates (its
   // lo + 1 is the hi to move); ties in t are resolved by |a|, then the smallest index.
-#ifdef ISF_OPT_FUSEMAX
-  const uint64_t gtm = warp_max_u64((uint64_t)__double_as_longlong(tmd));
-#else
-  uint64_t tm = 0;
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const uint64_t tb = ((mH >> r) & 1u) ? 0ull : (uint64_t)__double_as_longlong(t[r]);
-    tm = tb > tm ? tb : tm;
-  }
-  const uint64_t gtm = warp_max_u64(tm);
-#endif
-  uint32_t cm = 0;
-#pragma unroll
-  for (int r = 0; r < 16; ++r)
-    if (!((mH >> r) & 1u) && (uint64_t)__double_as_longlong(t[r]) == gtm) cm |= 1u << r;
-  const uint32_t ncand = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(cm));
-  uint32_t gidx;
-  if (ncand == 1) {
-    gidx = __reduce_min_sync(0xffffffffu, cm ? (uint32_t)(16 * lane + __ffs(cm) - 1) : 0xffffu);
-  } else {
-    uint64_t mk = 0;
-    int mi = 16;
-    double c16[16];
-    tmem_wait_st();
-    tmem_load16(tpark, c16);
+  // More than kMaxMoves moves (rare: TGV needs <= 4) go to the radix select.
+  constexpr int kMaxMoves = 6;
+  uint32_t mK = mH;
+  uint64_t SNc = SN;
+#pragma unroll 1
+  for (int mv = 0; mv < kMaxMoves; ++mv) {
+    uint64_t tm = 0;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const uint64_t kk = ((cm >> r) & 1u) ? abs_bits(c16[r]) + 1ull : 0ull;  // +1: zeros count
-      if (kk > mk) { mk = kk; mi = r; }
+      const uint64_t tb = ((mK >> r) & 1u) ? 0ull : (uint64_t)__double_as_longlong(t[r]);
+      tm = tb > tm ? tb : tm;
     }
-    const uint64_t gmk = warp_max_u64(mk);
-    gidx = __reduce_min_sync(0xffffffffu, (mk == gmk && mi < 16) ? (uint32_t)(16 * lane + mi) : 0xffffu);
-  }
-  const uint64_t h1 = gtm - C52 + 1ull;
-  if (gidx != 0xffffu && SN - h1 <= thr) {
-    s.mask = mH | (((int)(gidx >> 4) == lane) ? (1u << (gidx & 15)) : 0u);
-    s.hdisc = SN - h1;
-    return s;
+    const uint64_t gtm = warp_max_u64(tm);
+    uint32_t cm = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (!((mK >> r) & 1u) && (uint64_t)__double_as_longlong(t[r]) == gtm) cm |= 1u << r;
+    const uint32_t ncand = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(cm));
+    if (ncand == 0) break;  // defensive (cannot happen while SNc > thr)
+    uint32_t gidx;
+    if (ncand == 1) {
+      gidx = __reduce_min_sync(0xffffffffu, cm ? (uint32_t)(16 * lane + __ffs(cm) - 1) : 0xffffu);
+    } else {
+      uint64_t mk = 0;
+      int mi = 16;
+      double c16[16];
+      tmem_wait_st();
+      tmem_load16(tpark, c16);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint64_t kk = ((cm >> r) & 1u) ? abs_bits(c16[r]) + 1ull : 0ull;  // +1: zeros count
+        if (kk > mk) { mk = kk; mi = r; }
+      }
+      const uint64_t gmk = warp_max_u64(mk);
+      gidx = __reduce_min_sync(0xffffffffu, (mk == gmk && mi < 16) ? (uint32_t)(16 * lane + mi) : 0xffffu);
+    }
+    mK |= ((int)(gidx >> 4) == lane) ? (1u << (gidx & 15)) : 0u;
+    SNc -= gtm - C52 + 1ull;
+    if (SNc <= thr) {
+      s.mask = mK;
+      s.hdisc = SNc;
+      ISF_PATH(2);
+      return s;
+    }
   }
   uint64_t res[3];
   radix_select16(tpark, lane, thr, f, pre, hist, res);
@@ -366,6 +373,13 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
     if (kk > tstar || (kk == tstar && j < icut)) mk2 |= 1u << r;
   }
   s.mask = mk2;
+#ifdef ISF_PATHSTATS
+  {
+    const uint32_t kk = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(mk2)) - NH;
+    ISF_PATH(3);
+    ISF_PATH(kk < 8 ? 4 + kk : (kk < 16 ? 12 : (kk < 64 ? 13 : 14)));
+  }
+#endif
   s.hdisc = res[2];
   return s;
 }

@@ -821,6 +821,16 @@ __global__ void solver_standin_kernel(double* __restrict__ dst, const double* __
 }
 }  // namespace
 
+#ifdef ISF_PATHSTATS
+extern "C" int isf_debug_pathstats(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, isf::dev::g_pathstats, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(isf::dev::g_pathstats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 extern "C" int isf_lossy_solver_standin(double* d_dst, const double* d_src, const double* d_aux, uint64_t n,
                                         double alpha, void* cuda_stream) {
   if (!d_dst || !d_src || !d_aux || (n & 1) || (((uintptr_t)d_dst | (uintptr_t)d_src | (uintptr_t)d_aux) & 15))
