@@ -543,10 +543,10 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
 // --------------------------- block offsets / compact passes -----------------
 // off[b] = sum of counts of blocks < b (exclusive), off[B] = total.  CTA chunks of
 // 1024 blocks (4 per thread) chained by a decoupled look-back on ws.status with a
-// dynamic chunk claim (deadlock free).  With vslot != nullptr (compress) the kept
-// values of the chunk are then moved from their per-block slots into the packed
-// value region (flattened over the chunk: value i of the chunk by thread i % 256),
-// and the last CTA to finish reduces the statistics (fused finalize).
+// dynamic chunk claim (deadlock free).  Decompress (vslot == nullptr) stores off[];
+// compress instead moves each thread's four blocks' kept values from their per-block
+// slots into the packed value region (only off[B] is stored), and the last CTA to
+// finish reduces the statistics (fused finalize).
 constexpr int kOffThreads = 256;
 constexpr int kOffPerThread = 4;
 constexpr int kOffChunk = kOffThreads * kOffPerThread;
@@ -638,7 +638,6 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
   __shared__ uint64_t wsum[kOffThreads / 32];
   __shared__ uint64_t s_prefix;
   __shared__ uint32_t s_chunk;
-  __shared__ uint64_t s_off[kOffChunk + 1];
   __shared__ double s_red[4 * (kOffThreads / 32)];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t* counts = reinterpret_cast<const uint32_t*>(stream);
@@ -680,13 +679,8 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
     __syncthreads();
     const uint64_t e0 = s_prefix + wex + x - v;
     const uint64_t e1 = e0 + c4.x, e2 = e1 + c4.y, e3 = e2 + c4.z;
-    s_off[tid * 4 + 0] = e0;
-    s_off[tid * 4 + 1] = e1;
-    s_off[tid * 4 + 2] = e2;
-    s_off[tid * 4 + 3] = e3;
-    if (tid == kOffThreads - 1) s_off[kOffChunk] = e0 + v;
-    if (b0 < nblocks) {
-      // off[] is 8-byte aligned only: scalar stores
+    if (b0 < nblocks && !vslot) {
+      // decompress: per-block value offsets (off[] is 8-byte aligned only: scalar stores)
       off[b0] = e0;
       if (b0 + 1 < nblocks) off[b0 + 1] = e1;
       if (b0 + 2 < nblocks) off[b0 + 2] = e2;
@@ -700,19 +694,25 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
         for (uint64_t pb = nblocks; pb < ((nblocks + 3) & ~3ull); ++pb) wcounts[pb] = 0;  // pad to 16 B
       }
     }
-    __syncthreads();
-    if (vslot) {
-      const uint64_t first = s_off[0], nval = s_off[kOffChunk] - first;
-      if (first + nval <= cap_vals) {
-        for (uint64_t i = tid; i < nval; i += kOffThreads) {
-          // block t of the chunk holding value i: last t with s_off[t] - first <= i
-          int t = 0;
+    if (vslot && e0 + v <= cap_vals) {
+      // compress: move the thread's four blocks' kept values from their slots into
+      // the packed value region, four values of each block per round, all loads of a
+      // round in flight together (the slots are L2-resident for smooth fields)
+      const uint32_t cnt[4] = {c4.x, c4.y, c4.z, c4.w};
+      const uint64_t dof[4] = {e0, e1, e2, e3};
+      const uint32_t mx = ::max(::max(c4.x, c4.y), ::max(c4.z, c4.w));
+      for (uint32_t i = 0; i < mx; i += 4) {
+        double t[4][4];
 #pragma unroll
-          for (int step = kOffChunk / 2; step; step >>= 1)
-            if (t + step < kOffChunk && s_off[t + step] - first <= i) t += step;
-          const uint64_t bb = (uint64_t)chunk * kOffChunk + t;
-          vals[first + i] = vslot[bb * 512 + (first + i - s_off[t])];
-        }
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            t[q][k] = (i + k < cnt[q]) ? __ldcs(vslot + (b0 + q) * 512 + i + k) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (i + k < cnt[q]) vals[dof[q] + i + k] = t[q][k];
       }
     }
     __syncthreads();
