@@ -509,7 +509,10 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     const uint32_t mask = sel.nonfinite ? 0u : sel.mask;
     uint32_t kept;
     const uint32_t off = warp_exscan_small((uint32_t)__popc(mask), lane, kept);
-    if (lane == 0) counts[blk] = kept;  // the 16-B pad is zeroed by block_offsets8_kernel
+    if (lane == 0) {
+      counts[blk] = kept;  // the 16-B pad is zeroed by block_offsets8_kernel
+      if (kept) atomicAdd(reinterpret_cast<unsigned long long*>(A.ws.csum + (blk >> 10)), (unsigned long long)kept);
+    }
     masks16[blk * 32 + lane] = (uint16_t)mask;
     // kept values from the parked copy, written by their owner lane in index order:
     // one TMEM column pair per register slot r occupied in any lane
@@ -517,13 +520,19 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     if (um) {
       tmem_wait_st();
       double* dst = A.vslot + blk * 512 + off;
+      uint64_t pol;  // keep the slot lines in L2 for block_offsets8_kernel (the field streams evict_first)
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
       do {
         const int r = __ffs(um) - 1;
         um &= um - 1;
         uint32_t lo, hi;
         tmem_ld_32x32b_x2(tpark + 2u * (uint32_t)r, lo, hi);
         tmem_wait_ld();
-        if ((mask >> r) & 1u) *dst++ = __hiloint2double((int)hi, (int)lo);
+        if ((mask >> r) & 1u) {
+          asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(dst), "l"(((uint64_t)hi << 32) | lo), "l"(pol)
+                       : "memory");
+          ++dst;
+        }
       } while (um);
     }
     if (!sel.nonfinite && sel.T) {
@@ -543,13 +552,15 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
 // --------------------------- block offsets / compact passes -----------------
 // off[b] = sum of counts of blocks < b (exclusive), off[B] = total.  CTA chunks of
 // 1024 blocks (4 per thread) chained by a decoupled look-back on ws.status with a
-// dynamic chunk claim (deadlock free).  Decompress (vslot == nullptr) stores off[];
+// dynamic chunk claim (deadlock free); compress takes the chunk prefix from the
+// per-chunk sums compress8_kernel accumulated instead.  Decompress (vslot == nullptr) stores off[];
 // compress instead moves each thread's four blocks' kept values from their per-block
 // slots into the packed value region (only off[B] is stored), and the last CTA to
 // finish reduces the statistics (fused finalize).
 constexpr int kOffThreads = 256;
 constexpr int kOffPerThread = 4;
 constexpr int kOffChunk = kOffThreads * kOffPerThread;
+static_assert(kOffChunk == 1024, "compress8_kernel accumulates the chunk sums with blk >> 10");
 
 // Deterministic reduction of the per-warp partials into isf_lossy_stats by one CTA.
 __device__ void finalize_cta(const FinalizeArgs& A, double* s_red /* 4 * warps */) {
@@ -673,7 +684,18 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
       agg += wsum[w];
     }
     if (warp == 0) {
-      const uint64_t pre = warp_lookback(ws.status, chunk, agg, ws.epoch);
+      uint64_t pre;
+      if (vslot) {
+        // compress: compress8_kernel summed the kept counts per chunk, so the chunk's
+        // prefix is a plain sum (no look-back chain)
+        uint64_t a = 0;
+        for (uint32_t c = lane; c < chunk; c += 32) a += ws.csum[c];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        pre = a;
+      } else {
+        pre = warp_lookback(ws.status, chunk, agg, ws.epoch);
+      }
       if (lane == 0) s_prefix = pre;
     }
     __syncthreads();
@@ -706,8 +728,12 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            t[q][k] = (i + k < cnt[q]) ? __ldcs(vslot + (b0 + q) * 512 + i + k) : 0.0;
+          for (int k = 0; k < 4; k += 2)
+            if (i + k < cnt[q]) {  // slots are 16-B aligned: value pairs by 128-bit loads
+              const double2 d2 = __ldcs(reinterpret_cast<const double2*>(vslot + (b0 + q) * 512 + i + k));
+              t[q][k] = d2.x;
+              t[q][k + 1] = d2.y;
+            }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -717,7 +743,11 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
     }
     __syncthreads();
   }
-  if (fin.stats && last_cta(ws.counter + 1)) finalize_cta(fin, s_red);
+  if (last_cta(ws.counter + 1)) {
+    if (vslot)  // compress: clear the chunk sums for the next call
+      for (uint32_t c = threadIdx.x; c < nchunks; c += blockDim.x) ws.csum[c] = 0;
+    if (fin.stats) finalize_cta(fin, s_red);
+  }
 }
 
 // Two inverse lines (offsets O0, O1, stride S) of lx = 8 whose coefficients at

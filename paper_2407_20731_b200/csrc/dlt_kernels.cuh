@@ -18,6 +18,7 @@ struct Workspace {
   uint32_t epoch;
   uint32_t ntiles;
   uint32_t total_warps;        // warps (fast) or CTAs (generic) claiming tiles
+  uint64_t* csum = nullptr;    // lx = 8 compress: kept count per 1024-block chunk (zero between calls)
 };
 
 struct CompressArgs {

@@ -103,6 +103,7 @@ struct isf_lossy_plan {
   uint32_t P = 0, comps = 0;
   int sms = 0;
   uint64_t* status = nullptr;
+  uint64_t* csum = nullptr;  // per-chunk kept counts (lx = 8 compress), same capacity as status
   size_t status_cap = 0;
   double* partials = nullptr;
   size_t partials_cap = 0;  // slots of 4 doubles
@@ -139,9 +140,13 @@ namespace {
 int ensure(isf_lossy_plan* p, size_t ntiles, size_t nparts, size_t noff) {
   if (ntiles > p->status_cap) {
     if (p->status) cudaFree(p->status);
+    if (p->csum) cudaFree(p->csum);
+    p->csum = nullptr;
     size_t cap = std::max<size_t>(ntiles, 1024);
     CUDA_TRY(cudaMalloc(&p->status, cap * sizeof(uint64_t)));
     CUDA_TRY(cudaMemset(p->status, 0, cap * sizeof(uint64_t)));
+    CUDA_TRY(cudaMalloc(&p->csum, cap * sizeof(uint64_t)));
+    CUDA_TRY(cudaMemset(p->csum, 0, cap * sizeof(uint64_t)));
     p->status_cap = cap;
   }
   if (noff > p->toff_cap) {
@@ -313,6 +318,7 @@ int isf_lossy_plan_destroy(isf_lossy_plan* p) {
   if (!p) return 0;
   DeviceGuard dg(p->device);
   cudaFree(p->status);
+  cudaFree(p->csum);
   cudaFree(p->partials);
   cudaFree(p->toff);
   cudaFree(p->vslot);
@@ -379,6 +385,7 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   a.norm = error_norm;
   a.vslot = nullptr;
   a.ws = Workspace{p->status, p->partials, p->counter, p->flags, next_epoch(p, s), ntiles, 0};
+  a.ws.csum = p->csum;
   const uint64_t* total_ptr = nullptr;
   int launches = 2;
   uint64_t parts = ntiles;
