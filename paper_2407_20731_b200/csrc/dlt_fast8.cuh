@@ -552,8 +552,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
 // --------------------------- block offsets / compact passes -----------------
 // off[b] = sum of counts of blocks < b (exclusive), off[B] = total.  CTA chunks of
 // 1024 blocks (4 per thread) chained by a decoupled look-back on ws.status with a
-// dynamic chunk claim (deadlock free); compress takes the chunk prefix from the
-// per-chunk sums compress8_kernel accumulated instead.  Decompress (vslot == nullptr) stores off[];
+// dynamic chunk claim (deadlock free).  Decompress (vslot == nullptr) stores off[];
 // compress instead moves each thread's four blocks' kept values from their per-block
 // slots into the packed value region (only off[B] is stored), and the last CTA to
 // finish reduces the statistics (fused finalize).
@@ -684,18 +683,7 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
       agg += wsum[w];
     }
     if (warp == 0) {
-      uint64_t pre;
-      if (vslot) {
-        // compress: compress8_kernel summed the kept counts per chunk, so the chunk's
-        // prefix is a plain sum (no look-back chain)
-        uint64_t a = 0;
-        for (uint32_t c = lane; c < chunk; c += 32) a += ws.csum[c];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        pre = a;
-      } else {
-        pre = warp_lookback(ws.status, chunk, agg, ws.epoch);
-      }
+      const uint64_t pre = warp_lookback(ws.status, chunk, agg, ws.epoch);
       if (lane == 0) s_prefix = pre;
     }
     __syncthreads();
@@ -743,10 +731,87 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
     }
     __syncthreads();
   }
-  if (last_cta(ws.counter + 1)) {
-    if (vslot)  // compress: clear the chunk sums for the next call
-      for (uint32_t c = threadIdx.x; c < nchunks; c += blockDim.x) ws.csum[c] = 0;
+  if (fin.stats && last_cta(ws.counter + 1)) finalize_cta(fin, s_red);
+}
+
+// Compress epilogue: pack the kept values from their per-block slots into the value
+// region of the stream.  CTA c < nchunks owns chunk c (1024 blocks, one per thread):
+// its value offset is the sum of the per-chunk kept counts compress8_kernel
+// accumulated in csum (no look-back chain), the in-chunk offsets a block scan.  CTA
+// nchunks clears the other csum buffer (used by the next call) and reduces the
+// statistics, concurrently with the copies.
+constexpr int kCompactThreads = 1024;
+static_assert(kCompactThreads == kOffChunk, "one thread per block of a chunk");
+
+__global__ void __launch_bounds__(kCompactThreads) compact8_kernel(uint8_t* stream, uint64_t nblocks,
+                                                                  const uint64_t* csum, uint64_t* csum_next,
+                                                                  const double* vslot, double* vals,
+                                                                  uint64_t cap_vals, uint64_t* total_out,
+                                                                  uint32_t nclear, FinalizeArgs fin) {
+  __shared__ uint64_t s_w[kCompactThreads / 32];
+  __shared__ uint64_t s_prefix;
+  __shared__ double s_red[4 * (kCompactThreads / 32)];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t nchunks = (uint32_t)((nblocks + kOffChunk - 1) / kOffChunk);
+  const uint32_t chunk = blockIdx.x;
+  if (chunk == nchunks) {
+    for (uint32_t c = tid; c < nclear; c += kCompactThreads) csum_next[c] = 0;  // high-water mark of all calls
+    uint64_t a = 0;
+    for (uint32_t c = tid; c < nchunks; c += kCompactThreads) a += csum[c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) s_w[warp] = a;
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t t = 0;
+      for (int w = 0; w < kCompactThreads / 32; ++w) t += s_w[w];
+      *total_out = t;
+      if (t > cap_vals) atomicOr(fin.flags, kFlagOverflow);
+      __threadfence_block();
+    }
+    __syncthreads();
     if (fin.stats) finalize_cta(fin, s_red);
+    return;
+  }
+  if (warp == 0) {  // chunk prefix: the sum of the earlier chunks' kept counts
+    uint64_t a = 0;
+#pragma unroll 8
+    for (uint32_t c = lane; c < chunk; c += 32) a += csum[c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) s_prefix = a;
+  }
+  uint32_t* counts = reinterpret_cast<uint32_t*>(stream);
+  const uint64_t b = (uint64_t)chunk * kOffChunk + tid;
+  const uint32_t c = b < nblocks ? counts[b] : 0u;
+  uint32_t x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  uint64_t wex = 0;
+  for (int w = 0; w < warp; ++w) wex += s_w[w];
+  const uint64_t e = s_prefix + wex + x - c;
+  if (b + 1 == nblocks)  // zero the 16-B pad of the counts
+    for (uint64_t pb = nblocks; pb < ((nblocks + 3) & ~3ull); ++pb) counts[pb] = 0;
+  if (c && e + c <= cap_vals) {
+    const double* src = vslot + b * 512;
+    for (uint32_t i = 0; i < c; i += 8) {
+      double t[8];
+#pragma unroll
+      for (int k = 0; k < 8; k += 2)
+        if (i + k < c) {  // slots are 16-B aligned: value pairs by 128-bit loads
+          const double2 d2 = __ldcs(reinterpret_cast<const double2*>(src + i + k));
+          t[k] = d2.x;
+          t[k + 1] = d2.y;
+        }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (i + k < c) vals[e + i + k] = t[k];
+    }
   }
 }
 

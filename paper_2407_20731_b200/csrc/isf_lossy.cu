@@ -103,7 +103,9 @@ struct isf_lossy_plan {
   uint32_t P = 0, comps = 0;
   int sms = 0;
   uint64_t* status = nullptr;
-  uint64_t* csum = nullptr;  // per-chunk kept counts (lx = 8 compress), same capacity as status
+  uint64_t* csum = nullptr;  // per-chunk kept counts (lx = 8 compress): 2 x status_cap, double buffered
+  int csum_par = 0;
+  uint32_t csum_hw = 0;      // most chunks any call used (both buffers are clean beyond it)
   size_t status_cap = 0;
   double* partials = nullptr;
   size_t partials_cap = 0;  // slots of 4 doubles
@@ -145,8 +147,9 @@ int ensure(isf_lossy_plan* p, size_t ntiles, size_t nparts, size_t noff) {
     size_t cap = std::max<size_t>(ntiles, 1024);
     CUDA_TRY(cudaMalloc(&p->status, cap * sizeof(uint64_t)));
     CUDA_TRY(cudaMemset(p->status, 0, cap * sizeof(uint64_t)));
-    CUDA_TRY(cudaMalloc(&p->csum, cap * sizeof(uint64_t)));
-    CUDA_TRY(cudaMemset(p->csum, 0, cap * sizeof(uint64_t)));
+    p->csum_hw = 0;
+    CUDA_TRY(cudaMalloc(&p->csum, 2 * cap * sizeof(uint64_t)));
+    CUDA_TRY(cudaMemset(p->csum, 0, 2 * cap * sizeof(uint64_t)));
     p->status_cap = cap;
   }
   if (noff > p->toff_cap) {
@@ -385,7 +388,8 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   a.norm = error_norm;
   a.vslot = nullptr;
   a.ws = Workspace{p->status, p->partials, p->counter, p->flags, next_epoch(p, s), ntiles, 0};
-  a.ws.csum = p->csum;
+  a.ws.csum = p->csum + p->csum_par * p->status_cap;
+  if (fast) p->csum_hw = std::max<uint32_t>(p->csum_hw, nchunks8);
   const uint64_t* total_ptr = nullptr;
   int launches = 2;
   uint64_t parts = ntiles;
@@ -404,15 +408,14 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
     compress8_kernel<<<grid, kC8Warps * 32, kC8Smem, s>>>(a);
     CUDA_TRY(cudaGetLastError());
     parts = (uint64_t)grid * kC8Warps;
-    Workspace wo = a.ws;
-    wo.ntiles = nchunks8;
-    wo.total_warps = std::min<uint32_t>(nchunks8, (uint32_t)p->sms * 4);
     FinalizeArgs f{0, p->partials, parts, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
                    B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
-    block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>(
-        a.stream, B, p->toff, wo, p->vslot, reinterpret_cast<double*>(a.stream + a.val_off),
-        capacity > hdr ? (capacity - hdr) / 8 : 0, f);  // compaction + fused finalize
+    compact8_kernel<<<nchunks8 + 1, kCompactThreads, 0, s>>>(
+        a.stream, B, a.ws.csum, p->csum + (p->csum_par ^ 1) * p->status_cap, p->vslot,
+        reinterpret_cast<double*>(a.stream + a.val_off), capacity > hdr ? (capacity - hdr) / 8 : 0, p->toff + B,
+        p->csum_hw, f);  // compaction + concurrent finalize
     CUDA_TRY(cudaGetLastError());
+    p->csum_par ^= 1;
     p->last_launches = 2;
     return 0;
   }

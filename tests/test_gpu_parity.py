@@ -342,3 +342,16 @@ def test_linf_vector_field(native, oracle):
     blk = native.lossy_compress(f, PK.LossyConfig(1e-3, PK.ErrorNorm.RelativeLInf))
     rc, ref, _ = oracle.compress(v, P, 3, 1e-3, norm=1)
     assert rc == 0 and np.array_equal(blk.stream.cpu().numpy(), ref)
+
+
+def test_plan_reuse_varying_sizes(native, oracle):
+    """One plan, block counts that grow and shrink across calls: the double-buffered
+    per-chunk kept sums (compress8 -> compact8) must be clean for every call."""
+    P = 8
+    plan = native.get_plan(P, 1, 0)
+    for n_el in (5000, 1100, 70, 1100, 5000, 3000, 5000):
+        u = oracle.gen_spectral(P, n_el)
+        f = _field(P, 1, n_el, u)
+        blk = native.lossy_compress(f, native.LossyConfig(1e-3), plan=plan)
+        rc, ref, _ = oracle.compress(u, P, 1, 1e-3)
+        assert rc == 0 and np.array_equal(blk.stream.cpu().numpy(), ref), n_el
