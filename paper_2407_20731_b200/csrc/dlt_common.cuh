@@ -529,6 +529,12 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t ta, uint32_t (&r)[32
       : "r"(ta)
       : "memory");
 }
+__device__ __forceinline__ void tmem_st_16x256b_x4(uint32_t ta, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      ISF_R8(0), ISF_R8(8)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t ta, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"

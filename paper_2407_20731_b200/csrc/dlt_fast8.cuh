@@ -841,7 +841,7 @@ __device__ __forceinline__ void inv2_low8(double (&v)[N]) {
 
 // --------------------------- decompress -------------------------------------
 // stage: [96, ...) the block's values (16-B aligned bulk copy); [0, 96) unused
-constexpr int kD8Stage = 96 + 4096 + 32;
+constexpr int kD8Stage = 8 * 44 * 16;  // >= 96 + 4096 + 32 (values) and the re-layout planes
 constexpr int kD8StageBytes = (kD8Stage + 127) & ~127;
 constexpr int kD8WarpBytes = kF8Stages * kD8StageBytes + 128;  // stages | mbarriers
 constexpr int kD8Smem = kD8Warps * kD8WarpBytes;
@@ -863,6 +863,12 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
   uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kF8Stages * kD8StageBytes);
   const int kzp = lane >> 2, qp = lane & 3;
   const int q = lane & 3, y = lane >> 2;
+  // re-layout addresses: 16-B chunk (kz, ky, x pair xq) at kz * 44 + 4 ky + ky / 2 + xq,
+  // conflict free for the x-line stores, y-line loads / stores and z-line loads and
+  // affine in every loop index (immediate offsets from one base per role)
+  const int xoff = kzp * 44 + 9 * qp;            // x-lines: ky = 2 qp + kyi
+  const int yoff = kzp * 44 + qp;                // y-lines: + 4 ky + ky / 2
+  const int zoff = 4 * y + (y >> 1) + q;         // z-lines: + 44 z
   const uint64_t W = (uint64_t)gridDim.x * kD8Warps;
   const uint64_t gw = (uint64_t)blockIdx.x * kD8Warps + warp;
   const uint64_t B = A.nblocks;
@@ -959,12 +965,12 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
     for (int kyi = 0; kyi < 2; ++kyi)
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq)
-        sb[kzp * 32 + swz(kzp, (2 * qp + kyi) * 4 + qq)] = make_double2(v[kyi * 8 + 2 * qq], v[kyi * 8 + 2 * qq + 1]);
+        sb[xoff + 4 * kyi + qq] = make_double2(v[kyi * 8 + 2 * qq], v[kyi * 8 + 2 * qq + 1]);
     __syncwarp();
     if (Ky < 16u) {
 #pragma unroll
       for (int ky = 0; ky < 4; ++ky) {
-        const double2 t = sb[kzp * 32 + swz(kzp, ky * 4 + qp)];
+        const double2 t = sb[yoff + 4 * ky + (ky >> 1)];
         v[2 * ky] = t.x;
         v[2 * ky + 1] = t.y;
       }
@@ -973,7 +979,7 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
     } else {
 #pragma unroll
       for (int ky = 0; ky < 8; ++ky) {
-        const double2 t = sb[kzp * 32 + swz(kzp, ky * 4 + qp)];
+        const double2 t = sb[yoff + 4 * ky + (ky >> 1)];
         v[2 * ky] = t.x;
         v[2 * ky + 1] = t.y;
       }
@@ -981,13 +987,13 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
       lines<8, 2, 0, 1, 2, true>(v);
     }
 #pragma unroll
-    for (int yy = 0; yy < 8; ++yy) sb[kzp * 32 + swz(kzp, yy * 4 + qp)] = make_double2(v[2 * yy], v[2 * yy + 1]);
+    for (int yy = 0; yy < 8; ++yy) sb[yoff + 4 * yy + (yy >> 1)] = make_double2(v[2 * yy], v[2 * yy + 1]);
     __syncwarp();
     const bool lowz = Kz < 16u;
 #pragma unroll
     for (int z = 0; z < 8; ++z)
       if (z < 4 || !lowz) {
-        const double2 t = sb[z * 32 + swz(z, lane)];
+        const double2 t = sb[z * 44 + zoff];
         v[2 * z] = t.x;
         v[2 * z + 1] = t.y;
       }

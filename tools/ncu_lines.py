@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 
-def main(rep, kernel, so, blocks, top=40):
+def main(rep, kernel, so, blocks, top=40, mangled=None):
     sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                           capture_output=True, text=True).stdout
     rows = list(csv.reader(sass.splitlines()))
@@ -27,7 +27,8 @@ def main(rep, kernel, so, blocks, top=40):
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
     cub = [l for l in os.listdir(tmp) if l.endswith(".cubin")]
     dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub[0])], capture_output=True, text=True).stdout.split("\n")
-    start = [i for i, l in enumerate(dis) if l.startswith(".text.") and (str(len(kernel)) + kernel) in l][0]
+    key = mangled or (str(len(kernel.split("<")[0])) + kernel.split("<")[0])
+    start = [i for i, l in enumerate(dis) if l.startswith(".text.") and key in l][0]
     fl, offmap = None, {}
     for l in dis[start + 1:]:
         if l.startswith(".text."):
@@ -55,4 +56,4 @@ def main(rep, kernel, so, blocks, top=40):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]))
+    main(sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]), mangled=sys.argv[5] if len(sys.argv) > 5 else None)
