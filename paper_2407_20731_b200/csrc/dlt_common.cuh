@@ -470,6 +470,22 @@ __device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src,
       ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -541,6 +557,11 @@ __device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t ta, uint32_t (&r)[16
       : ISF_W8(0), ISF_W8(8)
       : "r"(ta)
       : "memory");
+}
+__device__ __forceinline__ void tmem_st_32x32b_x2(uint32_t ta, double d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(ta), "r"((uint32_t)__double2loint(d)),
+               "r"((uint32_t)__double2hiint(d))
+               : "memory");
 }
 __device__ __forceinline__ void tmem_ld_32x32b_x2(uint32_t ta, uint32_t& lo, uint32_t& hi) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(ta) : "memory");

@@ -420,10 +420,12 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   const uint32_t tbase = s_tmem;
   const uint32_t tx = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (uint32_t)(warp >> 2);
   const uint32_t tpark = tx + 32u;
+  const uint64_t pol_stream = l2_policy_evict_first();  // the field is read once
+  const uint64_t pol_keep = l2_policy_evict_last();     // value slots: re-read by compact8_kernel
   auto issue = [&](uint64_t blk, int st) {
     if (lane == 0 && blk < B) {
       mbar_arrive_tx(&bars[st], 4096u);
-      bulk_g2s_evict_first(wbase + st * kC8Stage, A.field + blk * 512, 4096u, &bars[st]);
+      bulk_g2s_hint(wbase + st * kC8Stage, A.field + blk * 512, 4096u, &bars[st], pol_stream);
     }
   };
 #pragma unroll
@@ -472,6 +474,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     // role; its double (g, j, h) of instruction g, rep j, half h holds
     // x2 = g, x1 = h, ky0 = j1, x0 = j0.
     {
+#ifndef ISF_T2_X2
       uint32_t r[32];
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
@@ -480,6 +483,13 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
         r[2 * c + 1] = (uint32_t)__double2hiint(v[2 * ky + x0]);
       }
       tmem_st_32x32b_x32(tx, r);
+#else
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int ky = ((c >> 1) & 1) * 4 + (c & 1) * 2 + (c >> 3), x0 = (c >> 2) & 1;
+        tmem_st_32x32b_x2(tx + 2u * c, v[2 * ky + x0]);
+      }
+#endif
       tmem_wait_st();
       uint32_t a0[16], a1[16];
       tmem_ld_16x256b_x4(tx, a0);
@@ -497,8 +507,10 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
 #ifndef ISF_EXP_NOXFORM
     lines<8, 1, 0, 8, 2, false>(v);  // x sweep: v[r] = coefficient 16*lane + r
 #endif
-    // park the coefficients in TMEM; the registers are then free for the selection
-    tmem_store16(tpark, v);
+    // park the coefficients in TMEM (one column pair per double: no register
+    // marshalling); the registers are then free for the selection
+#pragma unroll
+    for (int r = 0; r < 16; ++r) tmem_st_32x32b_x2(tpark + 2u * r, v[r]);
 #ifdef ISF_EXP_NOSEL
     Sel16 sel{0u, 1ull, 0ull, 0, false};
     if (__double_as_longlong(v[0]) == 0x1234) sel.mask = 1;
@@ -520,8 +532,6 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     if (um) {
       tmem_wait_st();
       double* dst = A.vslot + blk * 512 + off;
-      uint64_t pol;  // keep the slot lines in L2 for block_offsets8_kernel (the field streams evict_first)
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
       do {
         const int r = __ffs(um) - 1;
         um &= um - 1;
@@ -529,7 +539,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
         tmem_ld_32x32b_x2(tpark + 2u * (uint32_t)r, lo, hi);
         tmem_wait_ld();
         if ((mask >> r) & 1u) {
-          asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(dst), "l"(((uint64_t)hi << 32) | lo), "l"(pol)
+          asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(dst), "l"(((uint64_t)hi << 32) | lo), "l"(pol_keep)
                        : "memory");
           ++dst;
         }
