@@ -392,7 +392,8 @@ constexpr int kC8WarpBytes = kC8Stages * kC8Stage + 768 + 128;  // stages | hist
 constexpr int kC8Smem = kC8Warps * kC8WarpBytes;
 // TMEM columns per warp: [0, 32) y->x re-layout buffer, [32, 64) parked coefficients;
 // the four warps of a lane quadrant (warp % 4) sit side by side.
-constexpr uint32_t kC8TmemCols = 64u * (kC8Warps / 4);
+constexpr uint32_t pow2_ceil(uint32_t v) { return v <= 32u ? 32u : 2u * pow2_ceil((v + 1u) / 2u); }
+constexpr uint32_t kC8TmemCols = pow2_ceil(64u * (kC8Warps / 4));  // allocation: a power of 2 >= 32
 static_assert(kC8Warps % 4 == 0 && kC8TmemCols <= 512, "TMEM budget");
 
 __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A) {
