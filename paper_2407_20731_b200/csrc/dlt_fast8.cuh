@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     uint32_t kept;
     const uint32_t off = warp_exscan_small((uint32_t)__popc(mask), lane, kept);
     if (lane == 0) {
-      counts[blk] = kept;  // the 16-B pad is zeroed by block_offsets8_kernel
+      counts[blk] = kept;  // the 16-B pad is zeroed by compact8_kernel
       if (kept) atomicAdd(reinterpret_cast<unsigned long long*>(A.ws.csum + (blk >> 10)), (unsigned long long)kept);
     }
     masks16[blk * 32 + lane] = (uint16_t)mask;
@@ -561,12 +561,9 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
 }
 
 // --------------------------- block offsets / compact passes -----------------
-// off[b] = sum of counts of blocks < b (exclusive), off[B] = total.  CTA chunks of
-// 1024 blocks (4 per thread) chained by a decoupled look-back on ws.status with a
-// dynamic chunk claim (deadlock free).  Decompress (vslot == nullptr) stores off[];
-// compress instead moves each thread's four blocks' kept values from their per-block
-// slots into the packed value region (only off[B] is stored), and the last CTA to
-// finish reduces the statistics (fused finalize).
+// Decompress prologue: off[b] = sum of the stored counts of blocks < b (exclusive),
+// off[B] = total.  CTA chunks of 1024 blocks (4 per thread) chained by a decoupled
+// look-back on ws.status with a dynamic chunk claim (deadlock free).
 constexpr int kOffThreads = 256;
 constexpr int kOffPerThread = 4;
 constexpr int kOffChunk = kOffThreads * kOffPerThread;
@@ -653,9 +650,7 @@ __device__ __forceinline__ bool last_cta(uint32_t* done) {
 }
 
 __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8_t* stream, uint64_t nblocks,
-                                                                    uint64_t* off, Workspace ws,
-                                                                    const double* vslot, double* vals,
-                                                                    uint64_t cap_vals, FinalizeArgs fin) {
+                                                                    uint64_t* off, Workspace ws, FinalizeArgs fin) {
   __shared__ uint64_t wsum[kOffThreads / 32];
   __shared__ uint64_t s_prefix;
   __shared__ uint32_t s_chunk;
@@ -700,45 +695,12 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
     __syncthreads();
     const uint64_t e0 = s_prefix + wex + x - v;
     const uint64_t e1 = e0 + c4.x, e2 = e1 + c4.y, e3 = e2 + c4.z;
-    if (b0 < nblocks && !vslot) {
-      // decompress: per-block value offsets (off[] is 8-byte aligned only: scalar stores)
+    if (b0 < nblocks) {  // off[] is 8-byte aligned only: scalar stores
       off[b0] = e0;
       if (b0 + 1 < nblocks) off[b0 + 1] = e1;
       if (b0 + 2 < nblocks) off[b0 + 2] = e2;
       if (b0 + 3 < nblocks) off[b0 + 3] = e3;
-    }
-    if (b0 < nblocks && b0 + 4 >= nblocks) {
-      off[nblocks] = e0 + v;
-      if (vslot) {
-        if (e0 + v > cap_vals) atomicOr(ws.flags, kFlagOverflow);
-        uint32_t* wcounts = const_cast<uint32_t*>(counts);  // compress: the output stream
-        for (uint64_t pb = nblocks; pb < ((nblocks + 3) & ~3ull); ++pb) wcounts[pb] = 0;  // pad to 16 B
-      }
-    }
-    if (vslot && e0 + v <= cap_vals) {
-      // compress: move the thread's four blocks' kept values from their slots into
-      // the packed value region, four values of each block per round, all loads of a
-      // round in flight together (the slots are L2-resident for smooth fields)
-      const uint32_t cnt[4] = {c4.x, c4.y, c4.z, c4.w};
-      const uint64_t dof[4] = {e0, e1, e2, e3};
-      const uint32_t mx = ::max(::max(c4.x, c4.y), ::max(c4.z, c4.w));
-      for (uint32_t i = 0; i < mx; i += 4) {
-        double t[4][4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int k = 0; k < 4; k += 2)
-            if (i + k < cnt[q]) {  // slots are 16-B aligned: value pairs by 128-bit loads
-              const double2 d2 = __ldcs(reinterpret_cast<const double2*>(vslot + (b0 + q) * 512 + i + k));
-              t[q][k] = d2.x;
-              t[q][k + 1] = d2.y;
-            }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (i + k < cnt[q]) vals[dof[q] + i + k] = t[q][k];
-      }
+      if (b0 + 4 >= nblocks) off[nblocks] = e0 + v;
     }
     __syncthreads();
   }

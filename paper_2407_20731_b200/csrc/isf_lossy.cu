@@ -490,9 +490,8 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
     Workspace wo = a.ws;
     wo.ntiles = nchunks8;
     wo.total_warps = std::min<uint32_t>(nchunks8, (uint32_t)p->sms * 4);
-    FinalizeArgs none{};
     block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>((const uint8_t*)d_stream, B, p->toff, wo,
-                                                                 nullptr, nullptr, 0, none);
+                                                                  FinalizeArgs{});
     CUDA_TRY(cudaGetLastError());
     grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8d, (B + kD8Warps - 1) / kD8Warps);
     a.ws.total_warps = grid * kD8Warps;
