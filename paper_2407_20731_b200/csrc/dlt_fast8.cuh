@@ -893,8 +893,8 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
     ph ^= 1u << st;
     uint32_t m = mc;
     const uint32_t pc = (uint32_t)__popc(m);
-    const uint32_t inoff = warp_exscan_u32(pc, lane);
-    const uint32_t tot = __shfl_sync(0xffffffffu, inoff + pc, 31);
+    uint32_t tot;  // pc <= 16: five independent ballots instead of a dependent shuffle scan
+    const uint32_t inoff = warp_exscan_small(pc, lane, tot);
     // o1 - o0 is the block's stored count (block_offsets8_kernel scanned the counts)
     const bool ok = tot == o1 - o0 && A.val_off + 8 * o1 <= A.stream_bytes;
     if (!ok) {
