@@ -919,10 +919,18 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
     double v[16];
     const double* sv = sv0 + inoff;
     if (Kx < 16u) {  // warp-uniform: only kx 0..3 occupied
+      int o = 0;  // running value index (bits 4..7 and 12..15 are clear here)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        v[k] = ((m >> k) & 1u) ? sv[__popc(m & ((1u << k) - 1u))] : 0.0;
-        v[8 + k] = ((m >> (8 + k)) & 1u) ? sv[__popc(m & ((1u << (8 + k)) - 1u))] : 0.0;
+        const bool b = (m >> k) & 1u;
+        v[k] = b ? sv[o] : 0.0;
+        o += b;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool b = (m >> (8 + k)) & 1u;
+        v[8 + k] = b ? sv[o] : 0.0;
+        o += b;
       }
       __syncwarp();
       inv2_low8<1, 0, 8>(v);
