@@ -280,7 +280,8 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   s.T = T;
   const uint64_t thr = __umul64hi(T, eps_q);
   // kept-above-threshold set H: hi = lo + 1 > thr  <=>  lo >= thr  <=>  t >= 2^52 + thr
-  const double tthr = 4503599627370496.0 + (double)(thr < (1ull << 51) ? thr : (1ull << 51));
+  // 2^52 + min(thr, 2^51) exactly, from its bit pattern (no integer -> fp64 conversion)
+  const double tthr = __longlong_as_double((long long)(C52 + (thr < (1ull << 51) ? thr : (1ull << 51))));
   uint32_t mH = 0;
   uint64_t h0 = 0, h1s = 0;
 #if defined(ISF_OPT_HINT)

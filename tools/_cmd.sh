@@ -1,2 +1,2 @@
 timeout 300 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
-python tools/time_kernels.py varlib/exs.so varlib/dec.so 2>&1
+python tools/time_kernels.py varlib/dec.so varlib/tthr.so 2>&1
