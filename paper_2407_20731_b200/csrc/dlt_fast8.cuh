@@ -420,6 +420,8 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   __syncthreads();
   tmem_fence_after();
   const uint32_t tbase = s_tmem;
+  pdl_wait();  // the field / stream / workspace may come from the previous kernel
+  pdl_launch_dependents();
   const uint32_t tx = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (uint32_t)(warp >> 2);
   const uint32_t tpark = tx + 32u;
   const uint64_t pol_stream = l2_policy_evict_first();  // the field is read once
@@ -659,6 +661,8 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t* counts = reinterpret_cast<const uint32_t*>(stream);
   const uint32_t nchunks = (uint32_t)((nblocks + kOffChunk - 1) / kOffChunk);
+  pdl_wait();
+  pdl_launch_dependents();
   for (;;) {
     if (tid == 0) {
       const uint32_t c = atomicAdd(ws.counter, 1u);
@@ -728,6 +732,8 @@ __global__ void __launch_bounds__(kCompactThreads) compact8_kernel(uint8_t* stre
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nchunks = (uint32_t)((nblocks + kOffChunk - 1) / kOffChunk);
   const uint32_t chunk = blockIdx.x;
+  pdl_wait();
+  pdl_launch_dependents();
   if (chunk == nchunks) {
     for (uint32_t c = tid; c < nclear; c += kCompactThreads) csum_next[c] = 0;  // high-water mark of all calls
     uint64_t a = 0;
@@ -857,6 +863,8 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
     fence_mbar_init();
   }
   __syncwarp();
+  pdl_wait();
+  pdl_launch_dependents();
   // the TMA stage only carries the block's value range; offsets (from the counts) and
   // the lane's 16-bit mask word travel in registers, loaded two blocks ahead
   auto issue = [&](uint64_t blk, int st, uint64_t o0, uint64_t o1) {

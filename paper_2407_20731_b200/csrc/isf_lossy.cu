@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <utility>
 #include <mutex>
 #include <string>
 
@@ -174,6 +175,25 @@ uint32_t next_epoch(isf_lossy_plan* p, cudaStream_t s) {
     p->epoch = 1;
   }
   return p->epoch;
+}
+
+// Launch with programmatic dependent launch: the kernel may be scheduled while its
+// stream predecessor drains; every fast-path kernel starts with griddepcontrol.wait
+// (dev::pdl_wait), so it reads nothing before the predecessor has completed.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 template <int LX>
@@ -405,15 +425,15 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
     a.vslot = p->vslot;
     const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8c, (B + kC8Warps - 1) / kC8Warps);
     a.ws.total_warps = grid * kC8Warps;
-    compress8_kernel<<<grid, kC8Warps * 32, kC8Smem, s>>>(a);
+    CUDA_TRY(launch_pdl(compress8_kernel, grid, kC8Warps * 32, kC8Smem, s, a));
     CUDA_TRY(cudaGetLastError());
     parts = (uint64_t)grid * kC8Warps;
     FinalizeArgs f{0, p->partials, parts, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
                    B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
-    compact8_kernel<<<nchunks8 + 1, kCompactThreads, 0, s>>>(
-        a.stream, B, a.ws.csum, p->csum + (p->csum_par ^ 1) * p->status_cap, p->vslot,
-        reinterpret_cast<double*>(a.stream + a.val_off), capacity > hdr ? (capacity - hdr) / 8 : 0, p->toff + B,
-        p->csum_hw, f);  // compaction + concurrent finalize
+    CUDA_TRY(launch_pdl(compact8_kernel, nchunks8 + 1, kCompactThreads, 0, s, a.stream, B, (const uint64_t*)a.ws.csum,
+                        p->csum + (p->csum_par ^ 1) * p->status_cap, (const double*)p->vslot,
+                        reinterpret_cast<double*>(a.stream + a.val_off), capacity > hdr ? (capacity - hdr) / 8 : 0,
+                        p->toff + B, p->csum_hw, f));  // compaction + concurrent finalize
     CUDA_TRY(cudaGetLastError());
     p->csum_par ^= 1;
     p->last_launches = 2;
@@ -490,8 +510,8 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
     Workspace wo = a.ws;
     wo.ntiles = nchunks8;
     wo.total_warps = std::min<uint32_t>(nchunks8, (uint32_t)p->sms * 4);
-    block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>((const uint8_t*)d_stream, B, p->toff, wo,
-                                                                  FinalizeArgs{});
+    CUDA_TRY(launch_pdl(block_offsets8_kernel, wo.total_warps, kOffThreads, 0, s, (const uint8_t*)d_stream, B, p->toff,
+                        wo, FinalizeArgs{}));
     CUDA_TRY(cudaGetLastError());
     grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8d, (B + kD8Warps - 1) / kD8Warps);
     a.ws.total_warps = grid * kD8Warps;
@@ -499,8 +519,8 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
     FinalizeArgs f{1, p->partials, d_original ? parts : 0u, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
                    B * (uint64_t)p->P * p->P * p->P * 8, hdr, d_original ? 1 : 0};
     Decompress8Args a8{a, p->toff, f};
-    if (d_original) decompress8_kernel<true><<<grid, kD8Warps * 32, kD8Smem, s>>>(a8);  // + fused finalize
-    else decompress8_kernel<false><<<grid, kD8Warps * 32, kD8Smem, s>>>(a8);
+    if (d_original) CUDA_TRY(launch_pdl(decompress8_kernel<true>, grid, kD8Warps * 32, kD8Smem, s, a8));  // + finalize
+    else CUDA_TRY(launch_pdl(decompress8_kernel<false>, grid, kD8Warps * 32, kD8Smem, s, a8));
     CUDA_TRY(cudaGetLastError());
     p->last_launches = 2;
     return 0;
