@@ -8,6 +8,7 @@
 // SPEC.md:222-239.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace isf {
@@ -566,6 +567,30 @@ __device__ __forceinline__ void tmem_st_32x32b_x2(uint32_t ta, double d) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(ta), "r"((uint32_t)__double2loint(d)),
                "r"((uint32_t)__double2hiint(d))
                : "memory");
+}
+// 16 doubles -> column pairs 0..15 of the thread's lane: one asm block, so the base
+// address goes to a uniform register once (separate statements each get their own
+// R2UR) and every double stays in its own aligned register pair (no marshalling)
+__device__ __forceinline__ void tmem_park16(uint32_t ta, const double (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+0], {%1,%2};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+2], {%3,%4};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+4], {%5,%6};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+6], {%7,%8};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+8], {%9,%10};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+10], {%11,%12};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+12], {%13,%14};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+14], {%15,%16};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+16], {%17,%18};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+18], {%19,%20};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+20], {%21,%22};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+22], {%23,%24};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+24], {%25,%26};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+26], {%27,%28};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+28], {%29,%30};\n"
+      "tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+30], {%31,%32};\n"
+      ::"r"(ta), "r"((uint32_t)__double2loint(v[0])), "r"((uint32_t)__double2hiint(v[0])), "r"((uint32_t)__double2loint(v[1])), "r"((uint32_t)__double2hiint(v[1])), "r"((uint32_t)__double2loint(v[2])), "r"((uint32_t)__double2hiint(v[2])), "r"((uint32_t)__double2loint(v[3])), "r"((uint32_t)__double2hiint(v[3])), "r"((uint32_t)__double2loint(v[4])), "r"((uint32_t)__double2hiint(v[4])), "r"((uint32_t)__double2loint(v[5])), "r"((uint32_t)__double2hiint(v[5])), "r"((uint32_t)__double2loint(v[6])), "r"((uint32_t)__double2hiint(v[6])), "r"((uint32_t)__double2loint(v[7])), "r"((uint32_t)__double2hiint(v[7])), "r"((uint32_t)__double2loint(v[8])), "r"((uint32_t)__double2hiint(v[8])), "r"((uint32_t)__double2loint(v[9])), "r"((uint32_t)__double2hiint(v[9])), "r"((uint32_t)__double2loint(v[10])), "r"((uint32_t)__double2hiint(v[10])), "r"((uint32_t)__double2loint(v[11])), "r"((uint32_t)__double2hiint(v[11])), "r"((uint32_t)__double2loint(v[12])), "r"((uint32_t)__double2hiint(v[12])), "r"((uint32_t)__double2loint(v[13])), "r"((uint32_t)__double2hiint(v[13])), "r"((uint32_t)__double2loint(v[14])), "r"((uint32_t)__double2hiint(v[14])), "r"((uint32_t)__double2loint(v[15])), "r"((uint32_t)__double2hiint(v[15]))
+      : "memory");
 }
 __device__ __forceinline__ void tmem_ld_32x32b_x2(uint32_t ta, uint32_t& lo, uint32_t& hi) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(ta) : "memory");

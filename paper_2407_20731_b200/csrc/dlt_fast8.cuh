@@ -513,8 +513,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
 #endif
     // park the coefficients in TMEM (one column pair per double: no register
     // marshalling); the registers are then free for the selection
-#pragma unroll
-    for (int r = 0; r < 16; ++r) tmem_st_32x32b_x2(tpark + 2u * r, v[r]);
+    tmem_park16(tpark, v);
 #ifdef ISF_EXP_NOSEL
     Sel16 sel{0u, 1ull, 0ull, 0, false};
     if (__double_as_longlong(v[0]) == 0x1234) sel.mask = 1;
@@ -530,24 +529,19 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       if (kept) atomicAdd(reinterpret_cast<unsigned long long*>(A.ws.csum + (blk >> 10)), (unsigned long long)kept);
     }
     masks16[blk * 32 + lane] = (uint16_t)mask;
-    // kept values from the parked copy, written by their owner lane in index order:
-    // one TMEM column pair per register slot r occupied in any lane
-    uint32_t um = __reduce_or_sync(0xffffffffu, mask);
-    if (um) {
+    // kept values from the parked copy into the block's slot at their natural index
+    // (slot[j] = a_j for kept j): one TMEM load and sixteen predicated stores with
+    // immediate offsets; compact8_kernel gathers them in index order via the mask
+    if (__any_sync(0xffffffffu, mask != 0u)) {
       tmem_wait_st();
-      double* dst = A.vslot + blk * 512 + off;
-      do {
-        const int r = __ffs(um) - 1;
-        um &= um - 1;
-        uint32_t lo, hi;
-        tmem_ld_32x32b_x2(tpark + 2u * (uint32_t)r, lo, hi);
-        tmem_wait_ld();
-        if ((mask >> r) & 1u) {
-          asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(dst), "l"(((uint64_t)hi << 32) | lo), "l"(pol_keep)
+      double c16[16];
+      tmem_load16(tpark, c16);
+      double* dst = A.vslot + blk * 512 + 16 * lane;
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if ((mask >> r) & 1u)
+          asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(dst + r), "d"(c16[r]), "l"(pol_keep)
                        : "memory");
-          ++dst;
-        }
-      } while (um);
     }
     if (!sel.nonfinite && sel.T) {
       tot_acc += scale2((double)sel.T, -2 * sel.k);
@@ -721,7 +715,7 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
 constexpr int kCompactThreads = 1024;
 static_assert(kCompactThreads == kOffChunk, "one thread per block of a chunk");
 
-__global__ void __launch_bounds__(kCompactThreads) compact8_kernel(uint8_t* stream, uint64_t nblocks,
+__global__ void __launch_bounds__(kCompactThreads, 2) compact8_kernel(uint8_t* stream, uint64_t nblocks, uint64_t mask_off,
                                                                   const uint64_t* csum, uint64_t* csum_next,
                                                                   const double* vslot, double* vals,
                                                                   uint64_t cap_vals, uint64_t* total_out,
@@ -762,6 +756,7 @@ __global__ void __launch_bounds__(kCompactThreads) compact8_kernel(uint8_t* stre
     if (lane == 0) s_prefix = a;
   }
   uint32_t* counts = reinterpret_cast<uint32_t*>(stream);
+  const uint8_t* masks = stream + mask_off;  // 64 B (8 words) per block, 16-B aligned
   const uint64_t b = (uint64_t)chunk * kOffChunk + tid;
   const uint32_t c = b < nblocks ? counts[b] : 0u;
   uint32_t x = c;
@@ -778,19 +773,35 @@ __global__ void __launch_bounds__(kCompactThreads) compact8_kernel(uint8_t* stre
   if (b + 1 == nblocks)  // zero the 16-B pad of the counts
     for (uint64_t pb = nblocks; pb < ((nblocks + 3) & ~3ull); ++pb) counts[pb] = 0;
   if (c && e + c <= cap_vals) {
+    // compress8 left the kept values at their natural index in the block's slot:
+    // walk the block's 512-bit mask, four values in flight per round
     const double* src = vslot + b * 512;
-    for (uint32_t i = 0; i < c; i += 8) {
-      double t[8];
+    const ulonglong2* mk = reinterpret_cast<const ulonglong2*>(masks + b * 64);
+    uint64_t mw[8];
 #pragma unroll
-      for (int k = 0; k < 8; k += 2)
-        if (i + k < c) {  // slots are 16-B aligned: value pairs by 128-bit loads
-          const double2 d2 = __ldcs(reinterpret_cast<const double2*>(src + i + k));
-          t[k] = d2.x;
-          t[k + 1] = d2.y;
+    for (int w = 0; w < 4; ++w) {
+      const ulonglong2 q = mk[w];
+      mw[2 * w] = q.x;
+      mw[2 * w + 1] = q.y;
+    }
+    double* dst = vals + e;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      uint64_t m = mw[w];
+      while (m) {  // up to four set bits per round, their loads in flight together
+        int j[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          j[q] = m ? 64 * w + (__ffsll((long long)m) - 1) : -1;
+          m &= m - 1;
         }
+        double t[4];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (i + k < c) vals[e + i + k] = t[k];
+        for (int q = 0; q < 4; ++q) t[q] = j[q] >= 0 ? __ldcs(src + j[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (j[q] >= 0) *dst++ = t[q];
+      }
     }
   }
 }

@@ -430,7 +430,8 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
     parts = (uint64_t)grid * kC8Warps;
     FinalizeArgs f{0, p->partials, parts, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
                    B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
-    CUDA_TRY(launch_pdl(compact8_kernel, nchunks8 + 1, kCompactThreads, 0, s, a.stream, B, (const uint64_t*)a.ws.csum,
+    CUDA_TRY(launch_pdl(compact8_kernel, nchunks8 + 1, kCompactThreads, 0, s, a.stream, B, a.mask_off,
+                        (const uint64_t*)a.ws.csum,
                         p->csum + (p->csum_par ^ 1) * p->status_cap, (const double*)p->vslot,
                         reinterpret_cast<double*>(a.stream + a.val_off), capacity > hdr ? (capacity - hdr) / 8 : 0,
                         p->toff + B, p->csum_hw, f));  // compaction + concurrent finalize
