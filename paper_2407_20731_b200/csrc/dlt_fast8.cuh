@@ -528,7 +528,11 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       counts[blk] = kept;  // the 16-B pad is zeroed by compact8_kernel
       if (kept) atomicAdd(reinterpret_cast<unsigned long long*>(A.ws.csum + (blk >> 10)), (unsigned long long)kept);
     }
-    masks16[blk * 32 + lane] = (uint16_t)mask;
+    {  // mask words stay in L2 for compact8_kernel's gather (the field streams evict_first)
+      const uint16_t mw = (uint16_t)mask;
+      asm volatile("st.global.L2::cache_hint.b16 [%0], %1, %2;" ::"l"(masks16 + blk * 32 + lane), "h"(mw), "l"(pol_keep)
+                   : "memory");
+    }
     // kept values from the parked copy into the block's slot at their natural index
     // (slot[j] = a_j for kept j): one TMEM load and sixteen predicated stores with
     // immediate offsets; compact8_kernel gathers them in index order via the mask
