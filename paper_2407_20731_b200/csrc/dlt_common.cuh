@@ -33,10 +33,24 @@ __constant__ double c_w[kWTableSize];
 __constant__ double c_x[kWTableSize];
 __constant__ double c_bm[kWTableSize];  // RelativeLInf: max_i |B[i][k]| per lx (w_offset layout)
 
-template <int LX>
-__device__ __forceinline__ double Fm(int k, int i) { return c_ops[op_offset(LX) + k * LX + i]; }
-template <int LX>
-__device__ __forceinline__ double Bm(int i, int k) { return c_ops[op_offset(LX) + LX * LX + i * LX + k]; }
+// lx = 8: one private copy of F and of B per sweep (T = 0, 1, 2).  With a single
+// table the compiler keeps the 32 shared constants of the three sweeps live across
+// the loop and falls back to per-use LDC into vector registers; with a table per
+// sweep each sweep's constants go to uniform registers (LDCU) and feed the DFMAs
+// directly.  Same values, same arithmetic order: results are unchanged.
+__constant__ double c_f8[3][64];
+__constant__ double c_b8[3][64];
+
+template <int LX, int T = -1>
+__device__ __forceinline__ double Fm(int k, int i) {
+  if constexpr (LX == 8 && T >= 0) return c_f8[T][k * 8 + i];
+  else return c_ops[op_offset(LX) + k * LX + i];
+}
+template <int LX, int T = -1>
+__device__ __forceinline__ double Bm(int i, int k) {
+  if constexpr (LX == 8 && T >= 0) return c_b8[T][i * 8 + k];
+  else return c_ops[op_offset(LX) + LX * LX + i * LX + k];
+}
 template <int LX>
 __device__ __forceinline__ double Wg(int i) { return c_w[w_offset(LX) + i]; }
 
@@ -45,7 +59,7 @@ __device__ __forceinline__ double Wg(int i) { return c_w[w_offset(LX) + i]; }
 // forward: s_i = u_i + u_{n-1-i}, d_i = u_i - u_{n-1-i}; a_k = F[k][0]*v_0 then
 // ascending fma over the even (k even) / odd (k odd) half; middle node last.
 // ---------------------------------------------------------------------------
-template <int LX, int S, int O, int N>
+template <int LX, int S, int O, int N, int T = -1>
 __device__ __forceinline__ void fwd_line(double (&v)[N]) {
   constexpr int H = LX / 2;
   double s[H], d[H];
@@ -58,33 +72,33 @@ __device__ __forceinline__ void fwd_line(double (&v)[N]) {
   const double m = (LX & 1) ? v[O + H * S] : 0.0;
 #pragma unroll
   for (int k = 0; k < LX; ++k) {
-    double acc = __dmul_rn(Fm<LX>(k, 0), (k & 1) ? d[0] : s[0]);
+    double acc = __dmul_rn(Fm<LX, T>(k, 0), (k & 1) ? d[0] : s[0]);
 #pragma unroll
-    for (int i = 1; i < H; ++i) acc = __fma_rn(Fm<LX>(k, i), (k & 1) ? d[i] : s[i], acc);
-    if ((LX & 1) && !(k & 1)) acc = __fma_rn(Fm<LX>(k, H), m, acc);
+    for (int i = 1; i < H; ++i) acc = __fma_rn(Fm<LX, T>(k, i), (k & 1) ? d[i] : s[i], acc);
+    if ((LX & 1) && !(k & 1)) acc = __fma_rn(Fm<LX, T>(k, H), m, acc);
     v[O + k * S] = acc;
   }
 }
 
-template <int LX, int S, int O, int N>
+template <int LX, int S, int O, int N, int T = -1>
 __device__ __forceinline__ void inv_line(double (&v)[N]) {
   constexpr int H = LX / 2;
   double out[LX];
 #pragma unroll
   for (int i = 0; i < H; ++i) {
-    double E = __dmul_rn(Bm<LX>(i, 0), v[O]);
+    double E = __dmul_rn(Bm<LX, T>(i, 0), v[O]);
 #pragma unroll
-    for (int k = 2; k < LX; k += 2) E = __fma_rn(Bm<LX>(i, k), v[O + k * S], E);
-    double Od = __dmul_rn(Bm<LX>(i, 1), v[O + S]);
+    for (int k = 2; k < LX; k += 2) E = __fma_rn(Bm<LX, T>(i, k), v[O + k * S], E);
+    double Od = __dmul_rn(Bm<LX, T>(i, 1), v[O + S]);
 #pragma unroll
-    for (int k = 3; k < LX; k += 2) Od = __fma_rn(Bm<LX>(i, k), v[O + k * S], Od);
+    for (int k = 3; k < LX; k += 2) Od = __fma_rn(Bm<LX, T>(i, k), v[O + k * S], Od);
     out[i] = __dadd_rn(E, Od);
     out[LX - 1 - i] = __dsub_rn(E, Od);
   }
   if (LX & 1) {
-    double E = __dmul_rn(Bm<LX>(H, 0), v[O]);
+    double E = __dmul_rn(Bm<LX, T>(H, 0), v[O]);
 #pragma unroll
-    for (int k = 2; k < LX; k += 2) E = __fma_rn(Bm<LX>(H, k), v[O + k * S], E);
+    for (int k = 2; k < LX; k += 2) E = __fma_rn(Bm<LX, T>(H, k), v[O + k * S], E);
     out[H] = E;
   }
 #pragma unroll

@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     }
     __syncwarp();
 #ifndef ISF_EXP_NOXFORM
-    lines<8, 2, 0, 1, 2, false>(v);  // z sweep
+    lines8<0, 2, 0, 1, 2, false>(v);  // z sweep
 #endif
     // z -> y re-layout through the stage (in place): 16-B chunk c of plane kz at
     // kz * 33 + c (all reads of the stage are done)
@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     issue(blk + kC8Stages * W, st);  // the stage is free: refill it now
     st = (st + 1 == kC8Stages) ? 0 : st + 1;
 #ifndef ISF_EXP_NOXFORM
-    lines<8, 2, 0, 1, 2, false>(v);  // y sweep: v[2 ky + x0]
+    lines8<1, 2, 0, 1, 2, false>(v);  // y sweep: v[2 ky + x0]
 #endif
     // y -> x re-layout through TMEM: store 32x32b with column pair
     // c = (ky0, x0, ky2, ky1) [bits 3..0], re-read 16x256b at lanes 0 and 16.  Reader
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
         }
     }
 #ifndef ISF_EXP_NOXFORM
-    lines<8, 1, 0, 8, 2, false>(v);  // x sweep: v[r] = coefficient 16*lane + r
+    lines8<2, 1, 0, 8, 2, false>(v);  // x sweep: v[r] = coefficient 16*lane + r
 #endif
     // park the coefficients in TMEM (one column pair per double: no register
     // marshalling); the registers are then free for the selection
@@ -817,16 +817,16 @@ __global__ void __launch_bounds__(kCompactThreads, 2) compact8_kernel(uint8_t* s
 // nothing but the sign of zero: every intermediate keeps the real value of the
 // dense chain, sweep after sweep, and the +0 canonicalisation of the reconstruction
 // (applied by the oracle too) makes the bits identical.
-template <int S, int O0, int O1, int N>
+template <int S, int O0, int O1, int T, int N>
 __device__ __forceinline__ void inv2_low8(double (&v)[N]) {
   const double a0[4] = {v[O0], v[O0 + S], v[O0 + 2 * S], v[O0 + 3 * S]};
   const double a1[4] = {v[O1], v[O1 + S], v[O1 + 2 * S], v[O1 + 3 * S]};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const double e0 = __fma_rn(Bm<8>(i, 2), a0[2], __fma_rn(Bm<8>(i, 0), a0[0], 0.0));
-    const double d0 = __fma_rn(Bm<8>(i, 3), a0[3], __fma_rn(Bm<8>(i, 1), a0[1], 0.0));
-    const double e1 = __fma_rn(Bm<8>(i, 2), a1[2], __fma_rn(Bm<8>(i, 0), a1[0], 0.0));
-    const double d1 = __fma_rn(Bm<8>(i, 3), a1[3], __fma_rn(Bm<8>(i, 1), a1[1], 0.0));
+    const double e0 = __fma_rn(Bm<8, T>(i, 2), a0[2], __fma_rn(Bm<8, T>(i, 0), a0[0], 0.0));
+    const double d0 = __fma_rn(Bm<8, T>(i, 3), a0[3], __fma_rn(Bm<8, T>(i, 1), a0[1], 0.0));
+    const double e1 = __fma_rn(Bm<8, T>(i, 2), a1[2], __fma_rn(Bm<8, T>(i, 0), a1[0], 0.0));
+    const double d1 = __fma_rn(Bm<8, T>(i, 3), a1[3], __fma_rn(Bm<8, T>(i, 1), a1[1], 0.0));
     v[O0 + i * S] = __dadd_rn(e0, d0);
     v[O0 + (7 - i) * S] = __dsub_rn(e0, d0);
     v[O1 + i * S] = __dadd_rn(e1, d1);
@@ -957,13 +957,13 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
         o += b;
       }
       __syncwarp();
-      inv2_low8<1, 0, 8>(v);
+      inv2_low8<1, 0, 8, 0>(v);
     } else {
       int o = 0;
 #pragma unroll
       for (int r = 0; r < 16; ++r) v[r] = ((m >> r) & 1u) ? sv[o++] : 0.0;
       __syncwarp();
-      lines<8, 1, 0, 8, 2, true>(v);
+      lines8<0, 1, 0, 8, 2, true>(v);
     }
     double2* sb = reinterpret_cast<double2*>(sp);
 #pragma unroll
@@ -980,7 +980,7 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
         v[2 * ky + 1] = t.y;
       }
       __syncwarp();
-      inv2_low8<2, 0, 1>(v);
+      inv2_low8<2, 0, 1, 1>(v);
     } else {
 #pragma unroll
       for (int ky = 0; ky < 8; ++ky) {
@@ -989,7 +989,7 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
         v[2 * ky + 1] = t.y;
       }
       __syncwarp();
-      lines<8, 2, 0, 1, 2, true>(v);
+      lines8<1, 2, 0, 1, 2, true>(v);
     }
 #pragma unroll
     for (int yy = 0; yy < 8; ++yy) sb[yoff + 4 * yy + (yy >> 1)] = make_double2(v[2 * yy], v[2 * yy + 1]);
@@ -1009,7 +1009,7 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
     o0 = p0; o1 = p1;
     p0 = r0; p1 = r1;
     mc = mn; mn = mr;
-    if (lowz) inv2_low8<2, 0, 1>(v); else lines<8, 2, 0, 1, 2, true>(v);  // inverse z sweep
+    if (lowz) inv2_low8<2, 0, 1, 2>(v); else lines8<2, 2, 0, 1, 2, true>(v);  // inverse z sweep
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = __dadd_rn(v[r], 0.0);  // zeros as +0
     double2* dst = reinterpret_cast<double2*>(A.out + blk * 512) + lane;

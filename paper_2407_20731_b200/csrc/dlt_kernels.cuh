@@ -51,12 +51,17 @@ struct DecompressArgs {
 constexpr unsigned long long kFlagNonFinite = 1, kFlagShape = 2, kFlagOverflow = 4;
 
 // --------------------------- helpers ---------------------------------------
-template <int LX, int S, int O0, int DO, int CNT, bool INV, int N>
+template <int LX, int S, int O0, int DO, int CNT, bool INV, int N, int T = -1>
 __device__ __forceinline__ void lines(double (&v)[N]) {
   if constexpr (CNT > 0) {
-    if constexpr (INV) inv_line<LX, S, O0>(v); else fwd_line<LX, S, O0>(v);
-    lines<LX, S, O0 + DO, DO, CNT - 1, INV>(v);
+    if constexpr (INV) inv_line<LX, S, O0, N, T>(v); else fwd_line<LX, S, O0, N, T>(v);
+    lines<LX, S, O0 + DO, DO, CNT - 1, INV, N, T>(v);
   }
+}
+// lx = 8 sweep with its own constant table (see c_f8 / c_b8)
+template <int T, int S, int O0, int DO, int CNT, bool INV, int N>
+__device__ __forceinline__ void lines8(double (&v)[N]) {
+  lines<8, S, O0, DO, CNT, INV, N, T>(v);
 }
 template <int LX, int S, int O0, int DO1, int CNT1, int DO2, int CNT2, bool INV, int N>
 __device__ __forceinline__ void lines2(double (&v)[N]) {

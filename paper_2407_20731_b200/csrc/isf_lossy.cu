@@ -71,6 +71,15 @@ int init_device_constants(int device) {
   CUDA_TRY(cudaMemcpyToSymbol(c_ops, ops, sizeof ops));
   CUDA_TRY(cudaMemcpyToSymbol(c_w, ws, sizeof ws));
   CUDA_TRY(cudaMemcpyToSymbol(c_x, xs, sizeof xs));
+  {  // lx = 8: a private copy of F and B per sweep (dlt_common.cuh, c_f8 / c_b8)
+    double f8[3][64], b8[3][64];
+    for (int t = 0; t < 3; ++t) {
+      memcpy(f8[t], ops + op_offset(8), sizeof(double) * 64);
+      memcpy(b8[t], ops + op_offset(8) + 64, sizeof(double) * 64);
+    }
+    CUDA_TRY(cudaMemcpyToSymbol(c_f8, f8, sizeof f8));
+    CUDA_TRY(cudaMemcpyToSymbol(c_b8, b8, sizeof b8));
+  }
   static isf::crc::Tables crc_tables;
   static bool crc_built = false;
   if (!crc_built) { isf::crc::build_tables(crc_tables); crc_built = true; }
