@@ -24,10 +24,16 @@ namespace dev {
 #define ISF_C8_WARPS 16
 #endif
 #ifndef ISF_D8_WARPS
-#define ISF_D8_WARPS 16
+#define ISF_D8_WARPS 24
+#endif
+#ifndef ISF_D8E_WARPS
+#define ISF_D8E_WARPS 16
 #endif
 constexpr int kC8Warps = ISF_C8_WARPS;  // compress warps per CTA
-constexpr int kD8Warps = ISF_D8_WARPS;  // decompress warps per CTA
+constexpr int kD8Warps = ISF_D8_WARPS;    // decompress warps per CTA (plain decode: 68 registers)
+constexpr int kD8WarpsErr = ISF_D8E_WARPS;  // ... with the error report (more live state)
+template <bool ERR>
+__host__ __device__ constexpr int d8_warps() { return ERR ? kD8WarpsErr : kD8Warps; }
 constexpr int kF8Stages = 2;   // TMA ring depth per warp (decompress)
 #ifndef ISF_C8_STAGES
 #define ISF_C8_STAGES 2
@@ -836,10 +842,11 @@ __device__ __forceinline__ void inv2_low8(double (&v)[N]) {
 
 // --------------------------- decompress -------------------------------------
 // stage: [96, ...) the block's values (16-B aligned bulk copy); [0, 96) unused
-constexpr int kD8Stage = 8 * 44 * 16;  // >= 96 + 4096 + 32 (values) and the re-layout planes
+constexpr int kD8Stage = 8 * 36 * 16;  // >= 96 + 4096 + 32 (values) and the re-layout planes
 constexpr int kD8StageBytes = (kD8Stage + 127) & ~127;
 constexpr int kD8WarpBytes = kF8Stages * kD8StageBytes + 128;  // stages | mbarriers
-constexpr int kD8Smem = kD8Warps * kD8WarpBytes;
+template <bool ERR>
+__host__ __device__ constexpr int d8_smem() { return d8_warps<ERR>() * kD8WarpBytes; }
 
 struct Decompress8Args {
   DecompressArgs d;
@@ -850,7 +857,8 @@ struct Decompress8Args {
 // ERR: also read the original and accumulate the error report (separate instantiation
 // so the plain decode does not carry the accumulators' registers)
 template <bool ERR>
-__global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8Args P) {
+__global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decompress8Args P) {
+  constexpr int kNW = d8_warps<ERR>();
   const DecompressArgs& A = P.d;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -858,14 +866,14 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
   uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kF8Stages * kD8StageBytes);
   const int kzp = lane >> 2, qp = lane & 3;
   const int q = lane & 3, y = lane >> 2;
-  // re-layout addresses: 16-B chunk (kz, ky, x pair xq) at kz * 44 + 4 ky + ky / 2 + xq,
+  // re-layout addresses: 16-B chunk (kz, ky, x pair xq) at kz * 36 + 4 ky + ky / 2 + xq,
   // conflict free for the x-line stores, y-line loads / stores and z-line loads and
   // affine in every loop index (immediate offsets from one base per role)
-  const int xoff = kzp * 44 + 9 * qp;            // x-lines: ky = 2 qp + kyi
-  const int yoff = kzp * 44 + qp;                // y-lines: + 4 ky + ky / 2
-  const int zoff = 4 * y + (y >> 1) + q;         // z-lines: + 44 z
-  const uint64_t W = (uint64_t)gridDim.x * kD8Warps;
-  const uint64_t gw = (uint64_t)blockIdx.x * kD8Warps + warp;
+  const int xoff = kzp * 36 + 9 * qp;            // x-lines: ky = 2 qp + kyi
+  const int yoff = kzp * 36 + qp;                // y-lines: + 4 ky + ky / 2
+  const int zoff = 4 * y + (y >> 1) + q;         // z-lines: + 36 z
+  const uint64_t W = (uint64_t)gridDim.x * kNW;
+  const uint64_t gw = (uint64_t)blockIdx.x * kNW + warp;
   const uint64_t B = A.nblocks;
   const uint64_t sb_floor16 = A.stream_bytes & ~15ull;
   const double wxy0 = __dmul_rn(Wg<8>(2 * q), Wg<8>(y));
@@ -998,7 +1006,7 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
 #pragma unroll
     for (int z = 0; z < 8; ++z)
       if (z < 4 || !lowz) {
-        const double2 t = sb[z * 44 + zoff];
+        const double2 t = sb[z * 36 + zoff];
         v[2 * z] = t.x;
         v[2 * z + 1] = t.y;
       }
@@ -1050,7 +1058,7 @@ __global__ void __launch_bounds__(kD8Warps * 32) decompress8_kernel(Decompress8A
       A.ws.partials[gw * 4 + 3] = __longlong_as_double((long long)uinf);
     }
   }
-  __shared__ double s_red[4 * kD8Warps];
+  __shared__ double s_red[4 * kNW];
   if (last_cta(A.ws.counter + 1)) finalize_cta(P.fin, s_red);
 }
 

@@ -142,7 +142,7 @@ struct isf_lossy_plan {
   uint32_t* crc_chunks = nullptr;
   size_t crc_cap = 0;
   uint64_t* crc_n = nullptr;
-  int grid8c = 0, grid8d = 0, gridg = 0;
+  int grid8c = 0, grid8d = 0, grid8de = 0, gridg = 0;
   size_t smem_g = 0;
 };
 
@@ -333,13 +333,19 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
   build_operators((int)P, p->F, p->B, p->x, p->w);
   if (use_fast8(p)) {
     CUDA_TRY(cudaFuncSetAttribute(compress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
-    CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kD8Smem));
-    CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kD8Smem));
+    CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  d8_smem<false>()));
+    CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  d8_smem<true>()));
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel, kC8Warps * 32, kC8Smem));
     p->grid8c = p->sms * std::max(occ, 1);
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel<true>, kD8Warps * 32, kD8Smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel<false>, d8_warps<false>() * 32,
+                                                           d8_smem<false>()));
     p->grid8d = p->sms * std::max(occ, 1);
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel<true>, d8_warps<true>() * 32,
+                                                           d8_smem<true>()));
+    p->grid8de = p->sms * std::max(occ, 1);
   }
   CUDA_TRY(ensure(p, 1 << 16, 1 << 14, 1 << 16) == 0 ? cudaSuccess : cudaErrorMemoryAllocation);
   *out = p;
@@ -501,7 +507,8 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
   if (B >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
   const uint32_t ntiles = (uint32_t)B;
   const uint32_t nchunks8 = (ntiles + kOffChunk - 1) / kOffChunk;
-  const size_t nparts = fast ? (size_t)p->grid8d * kD8Warps : (size_t)p->sms * 16;
+  const size_t nparts = fast ? std::max<size_t>((size_t)p->grid8d * kD8Warps, (size_t)p->grid8de * kD8WarpsErr)
+                             : (size_t)p->sms * 16;
   if (int rc = ensure(p, fast ? nchunks8 : ntiles, nparts, fast ? B + 1 : 0)) return rc;
   DecompressArgs a;
   a.stream = (const uint8_t*)d_stream;
@@ -523,14 +530,17 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
     CUDA_TRY(launch_pdl(block_offsets8_kernel, wo.total_warps, kOffThreads, 0, s, (const uint8_t*)d_stream, B, p->toff,
                         wo, FinalizeArgs{}));
     CUDA_TRY(cudaGetLastError());
-    grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8d, (B + kD8Warps - 1) / kD8Warps);
-    a.ws.total_warps = grid * kD8Warps;
-    parts = grid * kD8Warps;
+    const int nw = d_original ? kD8WarpsErr : kD8Warps;
+    grid = (uint32_t)std::min<uint64_t>((uint64_t)(d_original ? p->grid8de : p->grid8d), (B + nw - 1) / nw);
+    a.ws.total_warps = grid * nw;
+    parts = grid * nw;
     FinalizeArgs f{1, p->partials, d_original ? parts : 0u, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
                    B * (uint64_t)p->P * p->P * p->P * 8, hdr, d_original ? 1 : 0};
     Decompress8Args a8{a, p->toff, f};
-    if (d_original) CUDA_TRY(launch_pdl(decompress8_kernel<true>, grid, kD8Warps * 32, kD8Smem, s, a8));  // + finalize
-    else CUDA_TRY(launch_pdl(decompress8_kernel<false>, grid, kD8Warps * 32, kD8Smem, s, a8));
+    if (d_original)  // + error report and fused finalize
+      CUDA_TRY(launch_pdl(decompress8_kernel<true>, grid, d8_warps<true>() * 32, d8_smem<true>(), s, a8));
+    else
+      CUDA_TRY(launch_pdl(decompress8_kernel<false>, grid, d8_warps<false>() * 32, d8_smem<false>(), s, a8));
     CUDA_TRY(cudaGetLastError());
     p->last_launches = 2;
     return 0;
