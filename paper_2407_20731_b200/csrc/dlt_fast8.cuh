@@ -334,6 +334,9 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
       tm = tb > tm ? tb : tm;
     }
     const uint64_t gtm = warp_max_u64(tm);
+    // every remaining move removes at most this hi: give up early (exactly) when the
+    // moves left cannot cover the excess (turbulent spectra need hundreds of moves)
+    if (SNc - thr > (uint64_t)(kMaxMoves - mv) * (gtm - C52 + 1ull)) break;
     uint32_t cm = 0;
 #pragma unroll
     for (int r = 0; r < 16; ++r)

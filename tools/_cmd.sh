@@ -1,4 +1,4 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
-python tools/time_kernels.py varlib/s36d24.so varlib/d24e16.so 2>&1
-python bench.py --no-e2e --no-cpu > gpurun_out/b.json 2>&1; python -c "
-import json; d=json.load(open('gpurun_out/b.json')); r=d['roofline']; print(d['value'], r['compress_gbs'], r['decompress_gbs'], r['step_frac'], d['async_insitu']['slowdown'])"
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
+python tools/time_kernels.py varlib/early.so 2>&1
+ISF_LOSSY_LIB=varlib/early.so timeout 600 python tools/lx_sweep.py 2>&1 | python -c "
+import json,sys; d=json.load(sys.stdin); [print(k, round(v['compress_gbs']), round(v['decompress_gbs'])) for k,v in d.items() if 'lx8' in k]"
