@@ -215,6 +215,152 @@ __device__ unsigned long long g_pathstats[16];
 #else
 #define ISF_PATH(P_) do {} while (0)
 #endif
+// ---------------------------------------------------------------------------
+// General-path exact selection, binned (the common general case for turbulent
+// spectra).  hi = lo + 1 is monotone in |a|, so the 204 bins
+// bin(hi) = 4 floor(log2 hi) + (next two bits of hi) are ordered like the discard
+// order.  One pass of native u32 shared atomics (three 21-bit digit planes) gives
+// the exact energy of every bin; the cut lies in the first bin whose cumulative sum
+// exceeds R.  If that bin holds <= 32 coefficients they are sorted across the warp
+// (one key per lane, bitonic) and the cut is found with a warp prefix sum of their
+// hi; ties at the cut key keep the smallest indices (SPEC.md:225 stable order).
+// Returns false (nothing written) when the cut bin is too crowded: the caller falls
+// back to radix_select16.  out = {t*, icut, discarded hi-sum}, as radix_select16.
+// smem: bins = 3 x 256 u32, cand = 32 u64.
+// ---------------------------------------------------------------------------
+constexpr int kSelBins = 256;
+__device__ __noinline__ bool select_bins16(uint32_t tpark, int lane, uint64_t R, double f, double pre,
+                                           uint32_t* bins, uint64_t* cand, uint64_t* out) {
+  uint64_t kk[16], hv[16];
+  uint32_t bn[16];
+  {
+    double v[16];
+    tmem_wait_st();
+    tmem_load16(tpark, v);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const double a = __dmul_rn(v[r], pre);
+      kk[r] = abs_bits(a);
+      hv[r] = e_lo(a, f) + 1ull;  // in [1, 2^51)
+      const uint32_t B = 63u - (uint32_t)__clzll((long long)hv[r]);
+      bn[r] = (B << 2) | (uint32_t)(((hv[r] << 2) >> B) & 3u);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 3 * kSelBins / 32; ++j) bins[lane + 32 * j] = 0u;
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    atomicAdd(&bins[bn[r]], (uint32_t)(hv[r] & 0x1FFFFFu));
+    atomicAdd(&bins[kSelBins + bn[r]], (uint32_t)((hv[r] >> 21) & 0x1FFFFFu));
+    atomicAdd(&bins[2 * kSelBins + bn[r]], (uint32_t)(hv[r] >> 42));
+  }
+  __syncwarp();
+  // lane l owns bins 8l .. 8l+7
+  uint64_t bs[8];
+  uint64_t lsum = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int b = 8 * lane + q;
+    bs[q] = (uint64_t)bins[b] + ((uint64_t)bins[kSelBins + b] << 21) + ((uint64_t)bins[2 * kSelBins + b] << 42);
+    lsum += bs[q];
+  }
+  uint64_t x = lsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  uint64_t run = x - lsum;  // exclusive prefix of this lane's first bin
+  uint32_t dloc = kSelBins;
+  uint64_t exloc = 0;
+#pragma unroll
+  for (int q = 7; q >= 0; --q) {  // first bin (lowest q) whose inclusive sum exceeds R
+    uint64_t pre_q = run;
+#pragma unroll
+    for (int w = 0; w < q; ++w) pre_q += bs[w];
+    if (pre_q + bs[q] > R) { dloc = 8 * lane + q; exloc = pre_q; }
+  }
+  const uint32_t d = __reduce_min_sync(0xffffffffu, dloc);
+  if (d == kSelBins) {  // everything fits: discard all (t* = largest key, none kept at it)
+    uint64_t mx = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) mx = kk[r] > mx ? kk[r] : mx;
+    out[0] = warp_max_u64(mx);
+    out[1] = 0;
+    out[2] = __shfl_sync(0xffffffffu, x, 31);
+    return true;
+  }
+  const uint64_t ex = __shfl_sync(0xffffffffu, exloc, (int)(d >> 3));
+  // candidates: the coefficients of bin d
+  uint32_t cm = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) cm |= (bn[r] == d) ? (1u << r) : 0u;
+  uint32_t ncand;
+  const uint32_t pos = warp_exscan_small((uint32_t)__popc(cm), lane, ncand);
+  if (ncand > 32) {
+    ISF_PATH(15);
+    return false;
+  }
+  __syncwarp();
+  {
+    uint32_t p = pos;
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if ((cm >> r) & 1u) cand[p++] = kk[r];
+  }
+  __syncwarp();
+  uint64_t key = lane < (int)ncand ? cand[lane] : ~0ull;
+  __syncwarp();
+  // bitonic sort of the 32 keys, ascending by lane
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, key, j);
+      const bool up = ((lane & k) == 0);
+      const bool lower = ((lane & j) == 0);
+      key = (lower == up) ? (o < key ? o : key) : (o > key ? o : key);
+    }
+  const uint64_t h = lane < (int)ncand ? e_lo(__longlong_as_double((long long)key), f) + 1ull : 0ull;
+  uint64_t cs = h;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t t = __shfl_up_sync(0xffffffffu, cs, o);
+    if (lane >= o) cs += t;
+  }
+  // first sorted candidate that does not fit: the cut (it exists: bin d overflows)
+  const uint64_t Rr = R - ex;
+  const uint32_t over = __ballot_sync(0xffffffffu, lane < (int)ncand && cs > Rr);
+  const int ic = __ffs(over) - 1;
+  const uint64_t K = __shfl_sync(0xffffffffu, key, ic);
+  const uint64_t dis = __shfl_sync(0xffffffffu, cs - h, ic);  // candidates before the cut
+  // discarded tied members at K: those sorted before the cut
+  const uint32_t tiedbefore = __popc(__ballot_sync(0xffffffffu, lane < ic && key == K));
+  uint32_t icut = 0xffffffffu;
+  if (tiedbefore) {
+    // keep the (gcount - tiedbefore) smallest indices among the coefficients with key K
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) cnt += (kk[r] == K);
+    const uint32_t gcount = __reduce_add_sync(0xffffffffu, cnt);
+    const uint32_t want = gcount - tiedbefore;
+    const uint32_t below = warp_exscan_u32(cnt, lane);
+    uint32_t mine = 0xffffffffu, seen = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (kk[r] == K) {
+        if (below + seen == want) mine = (uint32_t)(16 * lane + r);
+        ++seen;
+      }
+    icut = __reduce_min_sync(0xffffffffu, mine);
+  }
+  out[0] = K;
+  out[1] = icut;
+  out[2] = ex + dis;
+  return true;
+}
+
 struct Sel16 {
   uint32_t mask;   // kept bits of this lane's 16 coefficients
   uint64_t T;      // block total of lo energies
@@ -370,7 +516,9 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
     }
   }
   uint64_t res[3];
-  radix_select16(tpark, lane, thr, f, pre, hist, res);
+  if (!select_bins16(tpark, lane, thr, f, pre, reinterpret_cast<uint32_t*>(hist) + 64,
+                     reinterpret_cast<uint64_t*>(hist), res))
+    radix_select16(tpark, lane, thr, f, pre, hist, res);
   const uint64_t tstar = res[0];
   const uint32_t icut = (uint32_t)res[1];
   uint32_t mk2 = 0;
@@ -398,7 +546,11 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
 // stage: the block's 4 KiB as loaded by the TMA engine, re-used in place for the z -> y
 // re-layout with a plane stride of 33 16-B chunks (528 B; conflict free both ways)
 constexpr int kC8Stage = 33 * 8 * 16;
-constexpr int kC8WarpBytes = kC8Stages * kC8Stage + 768 + 128;  // stages | hist (3 x 64 u32) | mbarriers
+// stages | selection scratch (radix: 3 x 64 u32; binned: 32 u64 candidates, then
+// 3 x 256 u32 bins at byte 256) | mbarriers
+constexpr int kC8Scratch = 32 * 8 + 3 * kSelBins * 4;
+static_assert(kC8Scratch >= 768, "radix_select16 needs 3 x 64 u32");
+constexpr int kC8WarpBytes = kC8Stages * kC8Stage + kC8Scratch + 128;
 constexpr int kC8Smem = kC8Warps * kC8WarpBytes;
 // TMEM columns per warp: [0, 32) y->x re-layout buffer, [32, 64) parked coefficients;
 // the four warps of a lane quadrant (warp % 4) sit side by side.
@@ -412,7 +564,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned char* wbase = smem + warp * kC8WarpBytes;
   unsigned long long* hist = reinterpret_cast<unsigned long long*>(wbase + kC8Stages * kC8Stage);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kC8Stages * kC8Stage + 768);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kC8Stages * kC8Stage + kC8Scratch);
   const int yoff = (lane & 7) * 33 + (lane >> 3);  // y-line role (plane kz = l%8, x pair q = l/8)
   uint32_t* counts = reinterpret_cast<uint32_t*>(A.stream);
   uint16_t* masks16 = reinterpret_cast<uint16_t*>(A.stream + A.mask_off);
