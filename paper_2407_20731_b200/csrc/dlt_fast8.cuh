@@ -701,12 +701,24 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       tmem_wait_st();
       double c16[16];
       tmem_load16(tpark, c16);
-      double* dst = A.vslot + blk * 512 + 16 * lane;
+      // slot layout: natural index (j = 16 lane + r at j) for sparse blocks (<= 16 kept:
+      // the few kept values share sectors), [r][lane] for dense ones (every store a
+      // contiguous 256 B); compact8_kernel picks the same layout from the count
+      if (kept <= 16) {
+        double* dst = A.vslot + blk * 512 + 16 * lane;
 #pragma unroll
-      for (int r = 0; r < 16; ++r)
-        if ((mask >> r) & 1u)
-          asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(dst + r), "d"(c16[r]), "l"(pol_keep)
-                       : "memory");
+        for (int r = 0; r < 16; ++r)
+          if ((mask >> r) & 1u)
+            asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(dst + r), "d"(c16[r]), "l"(pol_keep)
+                         : "memory");
+      } else {
+        double* dst = A.vslot + blk * 512 + lane;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if ((mask >> r) & 1u)
+            asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(dst + 32 * r), "d"(c16[r]), "l"(pol_keep)
+                         : "memory");
+      }
     }
     if (!sel.nonfinite && sel.T) {
       tot_acc += scale2((double)sel.T, -2 * sel.k);
@@ -888,6 +900,9 @@ __global__ void __launch_bounds__(kCompactThreads, 2) compact8_kernel(uint8_t* s
   __shared__ uint64_t s_w[kCompactThreads / 32];
   __shared__ uint64_t s_prefix;
   __shared__ double s_red[4 * (kCompactThreads / 32)];
+  __shared__ uint64_t s_off[kCompactThreads];  // dense list: value offsets
+  __shared__ uint16_t s_dense[kCompactThreads];
+  __shared__ uint32_t s_ndense;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nchunks = (uint32_t)((nblocks + kOffChunk - 1) / kOffChunk);
   const uint32_t chunk = blockIdx.x;
@@ -921,7 +936,7 @@ __global__ void __launch_bounds__(kCompactThreads, 2) compact8_kernel(uint8_t* s
     if (lane == 0) s_prefix = a;
   }
   uint32_t* counts = reinterpret_cast<uint32_t*>(stream);
-  const uint8_t* masks = stream + mask_off;  // 64 B (8 words) per block, 16-B aligned
+  const uint16_t* masks16 = reinterpret_cast<const uint16_t*>(stream + mask_off);  // 32 words per block
   const uint64_t b = (uint64_t)chunk * kOffChunk + tid;
   const uint32_t c = b < nblocks ? counts[b] : 0u;
   uint32_t x = c;
@@ -934,39 +949,68 @@ __global__ void __launch_bounds__(kCompactThreads, 2) compact8_kernel(uint8_t* s
   __syncthreads();
   uint64_t wex = 0;
   for (int w = 0; w < warp; ++w) wex += s_w[w];
-  const uint64_t e = s_prefix + wex + x - c;
+  const uint64_t e = s_prefix + wex + x - c;  // the block's first value
   if (b + 1 == nblocks)  // zero the 16-B pad of the counts
     for (uint64_t pb = nblocks; pb < ((nblocks + 3) & ~3ull); ++pb) counts[pb] = 0;
-  if (c && e + c <= cap_vals) {
-    // compress8 left the kept values at their natural index in the block's slot:
-    // walk the block's 512-bit mask, four values in flight per round
-    const double* src = vslot + b * 512;
-    const ulonglong2* mk = reinterpret_cast<const ulonglong2*>(masks + b * 64);
-    uint64_t mw[8];
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const ulonglong2 q = mk[w];
-      mw[2 * w] = q.x;
-      mw[2 * w + 1] = q.y;
+  if (tid == 0) s_ndense = 0;
+  __syncthreads();
+  // Sparse blocks (<= 16 kept, slot in natural index order): one thread walks the
+  // block's mask.  Dense blocks (slot layout [r][lane]) go to a list that whole warps
+  // pack below (thread-serial copies of hundreds of values would dominate).
+  if (c > 16) {
+    if (e + c <= cap_vals) {
+      const uint32_t k = atomicAdd(&s_ndense, 1u);
+      s_dense[k] = (uint32_t)tid;
+      s_off[k] = e;
     }
+  } else if (c && e + c <= cap_vals) {
+    const double* src = vslot + b * 512;
+    const ulonglong2* mk = reinterpret_cast<const ulonglong2*>(masks16 + b * 32);
     double* dst = vals + e;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      uint64_t m = mw[w];
-      while (m) {  // up to four set bits per round, their loads in flight together
-        int j[4];
+    for (int w2 = 0; w2 < 4; ++w2) {
+      const ulonglong2 q2 = mk[w2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          j[q] = m ? 64 * w + (__ffsll((long long)m) - 1) : -1;
-          m &= m - 1;
+      for (int hw = 0; hw < 2; ++hw) {
+        uint64_t mm = hw ? q2.y : q2.x;
+        const int w = 2 * w2 + hw;
+        while (mm) {  // up to four set bits per round, their loads in flight together
+          int j[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            j[q] = mm ? 64 * w + (__ffsll((long long)mm) - 1) : -1;
+            mm &= mm - 1;
+          }
+          double t4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) t4[q] = j[q] >= 0 ? __ldcs(src + j[q]) : 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (j[q] >= 0) *dst++ = t4[q];
         }
-        double t[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) t[q] = j[q] >= 0 ? __ldcs(src + j[q]) : 0.0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (j[q] >= 0) *dst++ = t[q];
       }
+    }
+  }
+  __syncthreads();
+  // dense blocks: lane l owns the block's coefficients 16 l .. 16 l + 15 (mask word l),
+  // so the slot reads and the packed writes of a warp are both contiguous
+  const uint32_t nd = s_ndense;
+  for (uint32_t i = warp; i < nd; i += kCompactThreads / 32) {
+    const uint64_t bb = (uint64_t)chunk * kOffChunk + s_dense[i];
+    const uint32_t m = masks16[bb * 32 + lane];
+    uint32_t kept;
+    const uint32_t off = warp_exscan_small((uint32_t)__popc(m), lane, kept);
+    const double* src = vslot + bb * 512 + lane;
+    double* dst = vals + s_off[i] + off;
+    int k = 0;
+#pragma unroll
+    for (int h = 0; h < 16; h += 4) {  // four loads in flight, then their stores
+      double v[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) v[r] = ((m >> (h + r)) & 1u) ? __ldcs(src + 32 * (h + r)) : 0.0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if ((m >> (h + r)) & 1u) dst[k++] = v[r];
     }
   }
 }
