@@ -217,9 +217,8 @@ __device__ unsigned long long g_pathstats[16];
 #endif
 // ---------------------------------------------------------------------------
 // General-path exact selection, binned (the common general case for turbulent
-// spectra).  hi = lo + 1 is monotone in |a|, so the 204 bins
-// bin(hi) = 4 floor(log2 hi) + (next two bits of hi) are ordered like the discard
-// order.  One pass of native u32 shared atomics (three 21-bit digit planes) gives
+// spectra).  Any monotone function of the key |a| orders bins like the discard
+// order; 256 quarter-binades of |a| below the block maximum are used.  One pass of native u32 shared atomics (three 21-bit digit planes) gives
 // the exact energy of every bin; the cut lies in the first bin whose cumulative sum
 // exceeds R.  If that bin holds <= 32 coefficients they are sorted across the warp
 // (one key per lane, bitonic) and the cut is found with a warp prefix sum of their
@@ -242,9 +241,17 @@ __device__ __noinline__ bool select_bins16(uint32_t tpark, int lane, uint64_t R,
       const double a = __dmul_rn(v[r], pre);
       kk[r] = abs_bits(a);
       hv[r] = e_lo(a, f) + 1ull;  // in [1, 2^51)
-      const uint32_t B = 63u - (uint32_t)__clzll((long long)hv[r]);
-      bn[r] = (B << 2) | (uint32_t)(((hv[r] << 2) >> B) & 3u);
     }
+    // bins: quarter binades of |a| (exponent and the next two bits: kk >> 50, a
+    // monotone function of the key) counted down from the block maximum; the lowest
+    // 64 binades of |a| (128 of energy) share bin 0
+    uint32_t top = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) top = ::max(top, (uint32_t)(kk[r] >> 50));
+    top = __reduce_max_sync(0xffffffffu, top);
+    const int base = (int)top - (kSelBins - 1);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) bn[r] = (uint32_t)::max((int)(kk[r] >> 50) - base, 0);
   }
 #pragma unroll
   for (int j = 0; j < 3 * kSelBins / 32; ++j) bins[lane + 32 * j] = 0u;
