@@ -20,7 +20,7 @@ EXPORTS = (
     "isf_lossy_decompress_async", "isf_lossy_decompress", "isf_lossy_compress_host",
     "isf_lossy_decompress_host", "isf_lossy_allreduce", "isf_lossy_compression_ratio",
     "isf_lossy_last_error", "isf_lossy_error_code_name", "isf_lossy_plan_operators",
-    "isf_lossy_plan_last_launches", "isf_lossy_generate_tgv", "isf_lossy_generate_spectral",
+    "isf_lossy_plan_last_launches", "isf_lossy_plan_set_compress_mode", "isf_lossy_generate_tgv", "isf_lossy_generate_spectral",
     "isf_lossy_solver_standin", "isf_lossy_crc32", "isf_lossy_frame_async",
 )
 FRAME_OVERHEAD = 62  # ISF_FRAME_OVERHEAD: 48-B header + codec trailer (10 B) + CRC (4 B)
@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
         "isf_lossy_error_code_name": ([i32], ctypes.c_char_p),
         "isf_lossy_plan_operators": ([P, P, P, P, P], i32),
         "isf_lossy_plan_last_launches": ([P], i32),
+        "isf_lossy_plan_set_compress_mode": ([P, i32], i32),
         "isf_lossy_generate_tgv": ([P, P, u32, u32, u32, i32, f64, P], i32),
         "isf_lossy_generate_spectral": ([P, P, u64, u64, u64, P, P], i32),
         "isf_lossy_solver_standin": ([P, P, P, u64, f64, P], i32),

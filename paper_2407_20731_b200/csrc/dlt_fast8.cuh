@@ -559,13 +559,35 @@ constexpr int kC8Scratch = 32 * 8 + 3 * kSelBins * 4;
 static_assert(kC8Scratch >= 768, "radix_select16 needs 3 x 64 u32");
 constexpr int kC8WarpBytes = kC8Stages * kC8Stage + kC8Scratch + 128;
 constexpr int kC8Smem = kC8Warps * kC8WarpBytes;
-// TMEM columns per warp: [0, 32) y->x re-layout buffer, [32, 64) parked coefficients;
-// the four warps of a lane quadrant (warp % 4) sit side by side.
+// TMEM columns per warp: [0, 32) y->x re-layout buffer, then the parked coefficients
+// (one 32-column slot; three for the single-pass kernel, whose value writes trail the
+// selection by two rounds); the four warps of a lane quadrant (warp % 4) sit side by side.
 constexpr uint32_t pow2_ceil(uint32_t v) { return v <= 32u ? 32u : 2u * pow2_ceil((v + 1u) / 2u); }
-constexpr uint32_t kC8TmemCols = pow2_ceil(64u * (kC8Warps / 4));  // allocation: a power of 2 >= 32
-static_assert(kC8Warps % 4 == 0 && kC8TmemCols <= 512, "TMEM budget");
+template <bool SP>
+__host__ __device__ constexpr uint32_t c8_tmem_cols() { return pow2_ceil((SP ? 128u : 64u) * (kC8Warps / 4)); }
+static_assert(kC8Warps % 4 == 0 && c8_tmem_cols<true>() <= 512, "TMEM budget");
 
-__global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A) {
+__device__ void finalize_cta(const FinalizeArgs& A, double* s_red);
+__device__ __forceinline__ bool last_cta(uint32_t* done);
+
+// Single-pass compress (SP): no value slots and no compaction kernel.  A block's value
+// offset is (values of all earlier rounds) + (values of the earlier CTAs in its round) +
+// (values of the earlier warps of its CTA): each CTA publishes its round aggregate
+// (epoch-tagged) once its 16 warps have selected, and every warp writes the values of
+// its block of round i - 2 while it works on round i, from the coefficients it parked
+// in TMEM (three slots), by which time the round's aggregates are normally published.
+struct Sp8Args {
+  uint64_t* rstat;       // [round][cta] (epoch << 40) | kept count of the CTA's 16 blocks
+  uint32_t epoch;
+  uint32_t nrounds;      // ceil(B / W): every warp runs all rounds (empty ones too)
+  double* vals;          // the stream's value region
+  uint64_t cap_vals;
+  uint64_t* total_out;   // total kept (read by the finalize)
+  FinalizeArgs fin;
+};
+
+template <bool SP>
+__global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A, Sp8Args S) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t s_tmem;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -578,7 +600,16 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   const uint64_t W = (uint64_t)gridDim.x * kC8Warps;
   const uint64_t gw = (uint64_t)blockIdx.x * kC8Warps + warp;
   const uint64_t B = A.nblocks;
-  if (warp == 0) tmem_alloc<kC8TmemCols>(&s_tmem);
+  __shared__ uint32_t s_kept[4][kC8Warps];  // SP: per-warp kept counts of the last rounds
+  __shared__ uint32_t s_arrive[4];
+  __shared__ uint32_t s_rstate[4];  // SP: round-total slots (codes in deferred())
+  __shared__ uint64_t s_rtot[4], s_rpre[4];
+  __shared__ double s_red[4 * kC8Warps];
+  if (warp == 0) tmem_alloc<c8_tmem_cols<SP>()>(&s_tmem);
+  if (threadIdx.x < 4) {
+    s_arrive[threadIdx.x] = 0u;
+    s_rstate[threadIdx.x] = 2u * threadIdx.x + 2u;  // READY(q - 4): slot q first serves round q
+  }
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kC8Stages; ++s) mbar_init(&bars[s], 1);
@@ -590,8 +621,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   const uint32_t tbase = s_tmem;
   pdl_wait();  // the field / stream / workspace may come from the previous kernel
   pdl_launch_dependents();
-  const uint32_t tx = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (uint32_t)(warp >> 2);
-  const uint32_t tpark = tx + 32u;
+  const uint32_t tx = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (SP ? 128u : 64u) * (uint32_t)(warp >> 2);
   const uint64_t pol_stream = l2_policy_evict_first();  // the field is read once
   const uint64_t pol_keep = l2_policy_evict_last();     // value slots: re-read by compact8_kernel
   auto issue = [&](uint64_t blk, int st) {
@@ -605,7 +635,77 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   double tot_acc = 0.0, disc_acc = 0.0;
   int st = 0;
   uint32_t ph = 0;
-  for (uint64_t blk = gw; blk < B; blk += W) {
+  // SP state: masks / counts of the two rounds whose values are still to be written,
+  // and the value offset of the first block of round i - 2
+  uint32_t m1 = 0, m2 = 0, k1 = 0, k2 = 0;
+  uint64_t vbase = 0;
+  // SP: write the values of this warp's block of round j (mask mj, kept kj) from TMEM
+  auto deferred = [&](uint32_t j, uint32_t mj, uint32_t kj) {
+    // the round's totals over all CTAs: gathered once per CTA (by the first warp to
+    // need them) and shared through shared memory
+    volatile uint32_t* rs = s_rstate + (j & 3);
+    uint32_t claim = 0;
+    // slot codes: READY(r) = 2 r + 10, BUSY(r) = 2 r + 9; round j takes the slot over
+    // from round j - 4, which no warp of the CTA needs any more (bounded skew: this warp
+    // saw every warp of every CTA arrive at round j - 1)
+    if (lane == 0) claim = atomicCAS(const_cast<uint32_t*>(rs), 2u * j + 2u, 2u * j + 9u) == 2u * j + 2u;
+    claim = __shfl_sync(0xffffffffu, claim, 0);
+    if (claim) {
+      uint64_t tot = 0, pre = 0;
+      for (uint32_t c = lane; c < gridDim.x; c += 32) {
+        const uint64_t* wp = S.rstat + (uint64_t)j * gridDim.x + c;
+        uint64_t w = ld_relaxed(wp);
+        while ((uint32_t)(w >> 40) != S.epoch) {
+          __nanosleep(32);
+          w = ld_relaxed(wp);
+        }
+        const uint64_t a = w & ((1ull << 40) - 1);
+        tot += a;
+        pre += (c < blockIdx.x) ? a : 0ull;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        pre += __shfl_xor_sync(0xffffffffu, pre, o);
+      }
+      if (lane == 0) {
+        s_rtot[j & 3] = tot;
+        s_rpre[j & 3] = pre;
+        __threadfence_block();
+        *rs = 2u * j + 10u;  // READY(j)
+      }
+      __syncwarp();
+    } else {
+      while (*rs != 2u * j + 10u) __nanosleep(32);
+      __threadfence_block();
+    }
+    const uint64_t tot = *(volatile uint64_t*)&s_rtot[j & 3];
+    const uint64_t pre = *(volatile uint64_t*)&s_rpre[j & 3];
+    uint64_t pw = 0;  // earlier warps of this CTA (their counts are in: the CTA published)
+    for (int w = 0; w < warp; ++w) pw += s_kept[j & 3][w];
+    const uint64_t o0 = vbase + pre + pw;
+    vbase += tot;
+    if (kj == 0) return;
+    if (o0 + kj > S.cap_vals) {
+      if (lane == 0) atomicOr(A.ws.flags, kFlagOverflow);
+      return;
+    }
+    uint32_t kk;
+    const uint32_t lo = warp_exscan_small((uint32_t)__popc(mj), lane, kk);
+    tmem_wait_st();
+    double c16[16];
+    tmem_load16(tx + 32u + 32u * (j % 3u), c16);
+    double* dst = S.vals + o0 + lo;
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if ((mj >> r) & 1u) *dst++ = c16[r];
+  };
+  const uint32_t nrounds = SP ? S.nrounds : (gw < B ? (uint32_t)((B - gw + W - 1) / W) : 0u);
+  for (uint32_t it = 0; it < nrounds; ++it) {
+    const uint64_t blk = gw + (uint64_t)it * W;
+    const uint32_t tpark = tx + 32u + (SP ? 32u * (it % 3u) : 0u);
+    uint32_t mask = 0, kept = 0;
+    if (!SP || blk < B) {  // warp-uniform
     double2* sb = reinterpret_cast<double2*>(wbase + st * kC8Stage);
     mbar_wait(&bars[st], (ph >> st) & 1u);
     ph ^= 1u << st;
@@ -689,12 +789,11 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     const Sel16 sel = select16(v, lane, A.eps_q, hist, tpark);
 #endif
     if (sel.nonfinite && lane == 0) atomicOr(A.ws.flags, kFlagNonFinite);
-    const uint32_t mask = sel.nonfinite ? 0u : sel.mask;
-    uint32_t kept;
+    mask = sel.nonfinite ? 0u : sel.mask;
     const uint32_t off = warp_exscan_small((uint32_t)__popc(mask), lane, kept);
     if (lane == 0) {
-      counts[blk] = kept;  // the 16-B pad is zeroed by compact8_kernel
-      if (kept) atomicAdd(reinterpret_cast<unsigned long long*>(A.ws.csum + (blk >> 10)), (unsigned long long)kept);
+      counts[blk] = kept;  // the 16-B pad is zeroed by compact8_kernel / the last CTA
+      if (!SP && kept) atomicAdd(reinterpret_cast<unsigned long long*>(A.ws.csum + (blk >> 10)), (unsigned long long)kept);
     }
     {  // mask words stay in L2 for compact8_kernel's gather (the field streams evict_first)
       const uint16_t mw = (uint16_t)mask;
@@ -704,7 +803,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     // kept values from the parked copy into the block's slot at their natural index
     // (slot[j] = a_j for kept j): one TMEM load and sixteen predicated stores with
     // immediate offsets; compact8_kernel gathers them in index order via the mask
-    if (__any_sync(0xffffffffu, mask != 0u)) {
+    if (!SP && __any_sync(0xffffffffu, mask != 0u)) {
       tmem_wait_st();
       double c16[16];
       tmem_load16(tpark, c16);
@@ -731,14 +830,52 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       tot_acc += scale2((double)sel.T, -2 * sel.k);
       disc_acc += scale2((double)sel.hdisc, -2 * sel.k);
     }
+    (void)off;
+    }  // live block
+    if constexpr (SP) {
+      // this CTA's aggregate of round it: the last of its 16 warps publishes it
+      if (lane == 0) {
+        s_kept[it & 3][warp] = kept;
+        __threadfence_block();
+        if (atomicAdd(&s_arrive[it & 3], 1u) == kC8Warps - 1) {
+          __threadfence_block();
+          uint64_t agg = 0;
+          for (int w = 0; w < kC8Warps; ++w) agg += *(volatile uint32_t*)&s_kept[it & 3][w];
+          s_arrive[it & 3] = 0u;
+          st_relaxed(S.rstat + (uint64_t)it * gridDim.x + blockIdx.x, ((uint64_t)S.epoch << 40) | agg);
+        }
+      }
+      __syncwarp();
+      if (it >= 2) deferred(it - 2, m2, k2);
+      m2 = m1; k2 = k1;
+      m1 = mask; k1 = kept;
+    }
+  }
+  if constexpr (SP) {  // the last two rounds
+    if (nrounds >= 2) deferred(nrounds - 2, m2, k2);
+    if (nrounds >= 1) deferred(nrounds - 1, m1, k1);
   }
   if (lane == 0) {
     A.ws.partials[gw * 4 + 0] = tot_acc;
     A.ws.partials[gw * 4 + 1] = disc_acc;
   }
+  if constexpr (SP) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *S.total_out = vbase;  // every warp agrees on it
+    if (last_cta(A.ws.counter + 1)) {
+      if (threadIdx.x == 0) {
+        uint32_t* wcounts = counts;
+        for (uint64_t pb = B; pb < ((B + 3) & ~3ull); ++pb) wcounts[pb] = 0;  // pad to 16 B
+        *S.total_out = vbase;
+        if (vbase > S.cap_vals) atomicOr(A.ws.flags, kFlagOverflow);
+        __threadfence_block();
+      }
+      __syncthreads();
+      if (S.fin.stats) finalize_cta(S.fin, s_red);
+    }
+  }
   tmem_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<kC8TmemCols>(tbase);
+  if (warp == 0) tmem_dealloc<c8_tmem_cols<SP>()>(tbase);
 }
 
 // --------------------------- block offsets / compact passes -----------------

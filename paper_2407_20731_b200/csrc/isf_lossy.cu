@@ -116,6 +116,9 @@ struct isf_lossy_plan {
   uint64_t* csum = nullptr;  // per-chunk kept counts (lx = 8 compress): 2 x status_cap, double buffered
   int csum_par = 0;
   uint32_t csum_hw = 0;      // most chunks any call used (both buffers are clean beyond it)
+  uint64_t* rstat = nullptr;  // single-pass compress: [round][cta] epoch-tagged aggregates
+  size_t rstat_cap = 0;
+  bool use_sp = false;        // single-pass compress8 (isf_lossy_plan_set_compress_mode)
   size_t status_cap = 0;
   double* partials = nullptr;
   size_t partials_cap = 0;  // slots of 4 doubles
@@ -181,6 +184,7 @@ uint32_t next_epoch(isf_lossy_plan* p, cudaStream_t s) {
   p->epoch = (p->epoch + 1) & 0xffffffu;
   if (p->epoch == 0) {  // wrapped: clear stale descriptors
     cudaMemsetAsync(p->status, 0, p->status_cap * sizeof(uint64_t), s);
+    if (p->rstat) cudaMemsetAsync(p->rstat, 0, p->rstat_cap * sizeof(uint64_t), s);
     p->epoch = 1;
   }
   return p->epoch;
@@ -332,14 +336,19 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
   CUDA_TRY(cudaMallocHost(&p->h_stats, sizeof(isf_lossy_stats)));
   build_operators((int)P, p->F, p->B, p->x, p->w);
   if (use_fast8(p)) {
-    CUDA_TRY(cudaFuncSetAttribute(compress8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
+    CUDA_TRY(cudaFuncSetAttribute(compress8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
     CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   d8_smem<false>()));
     CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   d8_smem<true>()));
     int occ = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel, kC8Warps * 32, kC8Smem));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel<true>, kC8Warps * 32, kC8Smem));
     p->grid8c = p->sms * std::max(occ, 1);
+    CUDA_TRY(cudaFuncSetAttribute(compress8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
+    {
+      const char* e = getenv("ISF_C8_KERNEL");  // dev override of the default schedule
+      if (e && strcmp(e, "singlepass") == 0) p->use_sp = true;
+    }
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel<false>, d8_warps<false>() * 32,
                                                            d8_smem<false>()));
     p->grid8d = p->sms * std::max(occ, 1);
@@ -357,6 +366,7 @@ int isf_lossy_plan_destroy(isf_lossy_plan* p) {
   DeviceGuard dg(p->device);
   cudaFree(p->status);
   cudaFree(p->csum);
+  cudaFree(p->rstat);
   cudaFree(p->partials);
   cudaFree(p->toff);
   cudaFree(p->vslot);
@@ -385,6 +395,15 @@ int isf_lossy_plan_operators(const isf_lossy_plan* p, double* F, double* B, doub
 }
 
 int isf_lossy_plan_last_launches(const isf_lossy_plan* p) { return p ? p->last_launches : -1; }
+
+int isf_lossy_plan_set_compress_mode(isf_lossy_plan* p, int mode) {
+  if (int rc = check_plan(p)) return -rc;
+  if (mode != ISF_COMPRESS_TWO_PASS && mode != ISF_COMPRESS_SINGLE_PASS)
+    return -fail(ISF_E_INVALID_ARGUMENT, "unknown compress mode %d", mode);
+  const int prev = p->use_sp ? ISF_COMPRESS_SINGLE_PASS : ISF_COMPRESS_TWO_PASS;
+  p->use_sp = mode == ISF_COMPRESS_SINGLE_PASS;
+  return prev;
+}
 
 int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t n_elements, double max_error,
                              int error_norm, void* d_stream, uint64_t capacity, isf_lossy_stats* d_stats,
@@ -429,6 +448,31 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   int launches = 2;
   uint64_t parts = ntiles;
   if (fast) {
+    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8c, (B + kC8Warps - 1) / kC8Warps);
+    a.ws.total_warps = grid * kC8Warps;
+    parts = (uint64_t)grid * kC8Warps;
+    FinalizeArgs f{0, p->partials, parts, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
+                   B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
+    const uint64_t cap_vals = capacity > hdr ? (capacity - hdr) / 8 : 0;
+    if (p->use_sp) {
+      const uint64_t W = (uint64_t)grid * kC8Warps;
+      const uint32_t nrounds = (uint32_t)((B + W - 1) / W);
+      const size_t need = (size_t)nrounds * grid;
+      if (need > p->rstat_cap) {
+        if (p->rstat) cudaFree(p->rstat);
+        p->rstat = nullptr;
+        p->rstat_cap = 0;
+        CUDA_TRY(cudaMalloc(&p->rstat, need * sizeof(uint64_t)));
+        CUDA_TRY(cudaMemset(p->rstat, 0, need * sizeof(uint64_t)));
+        p->rstat_cap = need;
+      }
+      Sp8Args sp{p->rstat, a.ws.epoch, nrounds, reinterpret_cast<double*>(a.stream + a.val_off), cap_vals,
+                 p->toff + B, f};
+      CUDA_TRY(launch_pdl(compress8_kernel<true>, grid, kC8Warps * 32, kC8Smem, s, a, sp));
+      p->last_launches = 1;
+      return 0;
+    }
+    // two-pass: per-block value slots, packed by compact8_kernel
     const size_t slot_bytes = (size_t)B * 512 * sizeof(double);
     if (slot_bytes > p->vslot_cap) {
       if (p->vslot) cudaFree(p->vslot);
@@ -438,19 +482,11 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
       p->vslot_cap = slot_bytes;
     }
     a.vslot = p->vslot;
-    const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->grid8c, (B + kC8Warps - 1) / kC8Warps);
-    a.ws.total_warps = grid * kC8Warps;
-    CUDA_TRY(launch_pdl(compress8_kernel, grid, kC8Warps * 32, kC8Smem, s, a));
-    CUDA_TRY(cudaGetLastError());
-    parts = (uint64_t)grid * kC8Warps;
-    FinalizeArgs f{0, p->partials, parts, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
-                   B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
+    CUDA_TRY(launch_pdl(compress8_kernel<false>, grid, kC8Warps * 32, kC8Smem, s, a, Sp8Args{}));
     CUDA_TRY(launch_pdl(compact8_kernel, nchunks8 + 1, kCompactThreads, 0, s, a.stream, B, a.mask_off,
-                        (const uint64_t*)a.ws.csum,
-                        p->csum + (p->csum_par ^ 1) * p->status_cap, (const double*)p->vslot,
-                        reinterpret_cast<double*>(a.stream + a.val_off), capacity > hdr ? (capacity - hdr) / 8 : 0,
+                        (const uint64_t*)a.ws.csum, p->csum + (p->csum_par ^ 1) * p->status_cap,
+                        (const double*)p->vslot, reinterpret_cast<double*>(a.stream + a.val_off), cap_vals,
                         p->toff + B, p->csum_hw, f));  // compaction + concurrent finalize
-    CUDA_TRY(cudaGetLastError());
     p->csum_par ^= 1;
     p->last_launches = 2;
     return 0;

@@ -280,6 +280,18 @@ class LossyPlan:
     def last_launches(self) -> int:
         return int(self._lib.isf_lossy_plan_last_launches(self._h))
 
+    TWO_PASS, SINGLE_PASS = 0, 1
+
+    def set_compress_mode(self, mode: int) -> int:
+        """lx = 8 compress schedule (isf_lossy_plan_set_compress_mode): TWO_PASS
+        (default; slots + packing kernel) or SINGLE_PASS (values written in place two
+        rounds after their selection; faster for weakly compressible data).  Returns
+        the previous mode; the streams are identical either way."""
+        rc = int(self._lib.isf_lossy_plan_set_compress_mode(self._h, int(mode)))
+        if rc < 0:
+            raise IsfError(ErrorCode.InvalidArgument, f"unknown compress mode {mode}")
+        return rc
+
     # ---- raw device entry points (bench / in-situ use) ----
     def compress_async(self, values: torch.Tensor, n_elements: int, max_error: float,
                        stream_buf: torch.Tensor, stats_buf: torch.Tensor, cuda_stream=None):

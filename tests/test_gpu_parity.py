@@ -355,3 +355,35 @@ def test_plan_reuse_varying_sizes(native, oracle):
         blk = native.lossy_compress(f, native.LossyConfig(1e-3), plan=plan)
         rc, ref, _ = oracle.compress(u, P, 1, 1e-3)
         assert rc == 0 and np.array_equal(blk.stream.cpu().numpy(), ref), n_el
+
+
+@pytest.mark.parametrize("kind", ["tgv", "spectral_dense", "spectral"])
+def test_single_pass_schedule(native, oracle, kind):
+    """The single-pass lx = 8 compress (values written in place two rounds after their
+    selection, behind per-round CTA aggregates) gives the two-pass streams byte for byte,
+    including dense blocks, partial last rounds and repeated calls on one plan."""
+    import paper_2407_20731_b200 as PK
+    P = 8
+    plan = PK.LossyPlan(P, 1, 0)
+    assert plan.set_compress_mode(PK.LossyPlan.SINGLE_PASS) == PK.LossyPlan.TWO_PASS
+    try:
+        if kind == "tgv":
+            u, n_el, eps = oracle.gen_tgv(24, P, 0), 24 ** 3, 1e-3
+        elif kind == "spectral_dense":
+            u, n_el, eps = oracle.gen_spectral(P, 7001), 7001, 1e-5
+        else:
+            u, n_el, eps = oracle.gen_spectral(P, 3333), 3333, 1e-2
+        f = _field(P, 1, n_el, u)
+        rc, ref, _ = oracle.compress(u, P, 1, eps)
+        assert rc == 0
+        for _ in range(3):
+            blk = native.lossy_compress(f, native.LossyConfig(eps), plan=plan)
+            assert plan.last_launches() == 1
+            assert np.array_equal(blk.stream.cpu().numpy(), ref)
+        back = native.lossy_decompress(blk, f.shape)
+        rc, ob, _ = oracle.decompress(ref, P, 1, n_el)
+        assert np.allclose(back.values.cpu().numpy(), ob, rtol=0, atol=0)
+    finally:
+        plan.set_compress_mode(PK.LossyPlan.TWO_PASS)
+    with pytest.raises(PK.IsfError):
+        plan.set_compress_mode(7)
