@@ -46,6 +46,7 @@ struct DecompressArgs {
   double* out;
   const double* orig;
   Workspace ws;
+  const uint64_t* off = nullptr;  // per-block value offsets (block_offsets8_kernel); else look-back
 };
 
 constexpr unsigned long long kFlagNonFinite = 1, kFlagShape = 2, kFlagOverflow = 4;
@@ -389,7 +390,8 @@ __global__ void __launch_bounds__(kGenThreads) decompress_generic(DecompressArgs
       }
       const LaneGroup<32> g;
       pc = g.sum(pc);
-      const uint64_t prefix = warp_lookback(A.ws.status, tile, cnt, A.ws.epoch);
+      // offsets precomputed by block_offsets8_kernel (no serial look-back chain)
+      const uint64_t prefix = A.off ? A.off[blk] : warp_lookback(A.ws.status, tile, cnt, A.ws.epoch);
       bool bad = pc != cnt || prefix + cnt > nvals_avail;
       if (lane == 0) {
         if (bad) atomicOr(A.ws.flags, kFlagShape);

@@ -545,7 +545,7 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
   const uint32_t nchunks8 = (ntiles + kOffChunk - 1) / kOffChunk;
   const size_t nparts = fast ? std::max<size_t>((size_t)p->grid8d * kD8Warps, (size_t)p->grid8de * kD8WarpsErr)
                              : (size_t)p->sms * 16;
-  if (int rc = ensure(p, fast ? nchunks8 : ntiles, nparts, fast ? B + 1 : 0)) return rc;
+  if (int rc = ensure(p, std::max<uint32_t>(nchunks8, 1), nparts, B + 1)) return rc;
   DecompressArgs a;
   a.stream = (const uint8_t*)d_stream;
   a.stream_bytes = stream_bytes;
@@ -581,6 +581,16 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
     p->last_launches = 2;
     return 0;
   } else {
+    // value offsets from the stored counts first (the same scan as the lx = 8 path)
+    Workspace wo = a.ws;
+    wo.ntiles = nchunks8;
+    wo.total_warps = std::min<uint32_t>(nchunks8, (uint32_t)p->sms * 4);
+    block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>((const uint8_t*)d_stream, B, p->toff, wo,
+                                                                  FinalizeArgs{});
+    CUDA_TRY(cudaGetLastError());
+    a.off = p->toff;
+    total_ptr = p->toff + B;
+    launches = 3;
     if (int rc = dispatch_decompress_generic(AllLx{}, (int)p->P, p, a, s, &grid)) return rc;
     parts = grid;
   }
