@@ -321,8 +321,14 @@ __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) 
       for (int w = lane; w < W; w += 32) nk += __popcll(maskw[w]);
       const LaneGroup<32> g;
       nk = g.sum(nk);
-      const uint64_t prefix = warp_lookback(A.ws.status, tile, nk, A.ws.epoch);
-      const bool fits = A.val_off + 8 * (prefix + nk) <= A.cap;
+      // slot mode (vslot): values at their natural index in the block's slot, packed
+      // afterwards (compact_generic_kernel); else a per-block look-back chain
+      uint64_t prefix = 0;
+      bool fits = true;
+      if (!A.vslot) {
+        prefix = warp_lookback(A.ws.status, tile, nk, A.ws.epoch);
+        fits = A.val_off + 8 * (prefix + nk) <= A.cap;
+      }
       if (lane == 0) {
         counts[blk] = nk;
         if (blk + 1 == A.nblocks) for (uint64_t pb = A.nblocks; pb < ((A.nblocks + 3) & ~3ull); ++pb) counts[pb] = 0;
@@ -335,7 +341,11 @@ __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) 
       for (int w = lane; w < W; w += 32) masks[blk * W + w] = maskw[w];
     }
     __syncthreads();
-    if (misc[2]) {
+    if (A.vslot) {
+      double* slot = A.vslot + blk * (uint64_t)N3;
+      for (int p = tid; p < N3; p += kGenThreads)
+        if ((maskw[p >> 6] >> (p & 63)) & 1ull) slot[p] = u[p];
+    } else if (misc[2]) {
       // kept values in ascending index: rank = popcount of lower mask bits
       const uint64_t prefix = misc[1];
       for (int p = tid; p < N3; p += kGenThreads) {
@@ -346,6 +356,36 @@ __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) 
           vals[prefix + rank] = u[p];
         }
       }
+    }
+  }
+}
+
+// Generic compress epilogue: pack the slots (natural index, N3 doubles per block) into
+// the value region.  One warp per block, one 64-bit mask word at a time: lane l moves
+// the word's bits 2l and 2l + 1 (rank = popcount of the lower bits), so reads and
+// writes stay contiguous for dense blocks and all-zero words cost one test.
+__global__ void __launch_bounds__(256) compact_generic_kernel(const uint8_t* stream, uint64_t nblocks,
+                                                            uint64_t mask_off, int W, int N3, const uint64_t* off,
+                                                            const double* vslot, double* vals, uint64_t cap_vals,
+                                                            unsigned long long* flags) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t* masks = reinterpret_cast<const uint64_t*>(stream + mask_off);
+  const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t b = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nblocks; b += nw) {
+    const uint64_t e = off[b], cnt = off[b + 1] - e;
+    if (b + 1 == nblocks && lane == 0 && off[nblocks] > cap_vals) atomicOr(flags, kFlagOverflow);
+    if (cnt == 0 || e + cnt > cap_vals) continue;  // warp-uniform
+    const double* src = vslot + b * (uint64_t)N3;
+    uint64_t base = e;
+    const int p2 = 2 * lane;  // this lane's two bits of every 64-bit mask word
+    for (int w = 0; w < W; ++w) {
+      const uint64_t m = masks[b * W + w];  // same word for the whole warp
+      if (m == 0) continue;
+      const uint32_t r0 = (uint32_t)__popcll(m & ((1ull << p2) - 1ull));
+      const uint32_t b0 = (uint32_t)(m >> p2) & 1u, b1 = (uint32_t)(m >> (p2 + 1)) & 1u;
+      if (b0) vals[base + r0] = __ldcs(src + 64 * w + p2);
+      if (b1) vals[base + r0 + b0] = __ldcs(src + 64 * w + p2 + 1);
+      base += (uint32_t)__popcll(m);
     }
   }
 }

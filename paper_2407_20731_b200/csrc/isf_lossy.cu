@@ -428,7 +428,7 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   const uint32_t ntiles = (uint32_t)B;  // generic: one tile per block; fast: one warp per block
   const uint32_t nchunks8 = (ntiles + kOffChunk - 1) / kOffChunk;
   const size_t nparts = fast ? (size_t)p->grid8c * kC8Warps : (size_t)ntiles;
-  if (int rc = ensure(p, fast ? nchunks8 : ntiles, nparts, fast ? B + 1 : 0)) return rc;
+  if (int rc = ensure(p, fast ? nchunks8 : ntiles, nparts, B + 1)) return rc;
   CompressArgs a;
   a.field = d_field;
   a.nblocks = B;
@@ -491,7 +491,34 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
     p->last_launches = 2;
     return 0;
   }
+  // generic: kept values to per-block slots, then the count scan and a packing pass
+  // (no per-block look-back chain)
+  {
+    const size_t slot_bytes = (size_t)B * p->P * p->P * p->P * sizeof(double);
+    if (slot_bytes > p->vslot_cap) {
+      if (p->vslot) cudaFree(p->vslot);
+      p->vslot = nullptr;
+      p->vslot_cap = 0;
+      CUDA_TRY(cudaMalloc(&p->vslot, slot_bytes));
+      p->vslot_cap = slot_bytes;
+    }
+    a.vslot = p->vslot;
+  }
   if (int rc = dispatch_compress_generic(AllLx{}, (int)p->P, p, a, s)) return rc;
+  {
+    Workspace wo = a.ws;
+    wo.ntiles = nchunks8;
+    wo.total_warps = std::min<uint32_t>(nchunks8, (uint32_t)p->sms * 4);
+    block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>(a.stream, B, p->toff, wo, FinalizeArgs{});
+    CUDA_TRY(cudaGetLastError());
+    const int n3 = (int)(p->P * p->P * p->P);
+    compact_generic_kernel<<<p->sms * 8, 256, 0, s>>>(a.stream, B, a.mask_off, (n3 + 63) / 64, n3, p->toff, p->vslot,
+                                                     reinterpret_cast<double*>(a.stream + a.val_off),
+                                                     capacity > hdr ? (capacity - hdr) / 8 : 0, p->flags);
+    CUDA_TRY(cudaGetLastError());
+    total_ptr = p->toff + B;
+    launches = 4;
+  }
   FinalizeArgs f{0, p->partials, parts, p->status, total_ptr, ntiles, p->flags, d_stats, B,
                  B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
   finalize_kernel<<<1, kFinThreads, 0, s>>>(f);
