@@ -481,14 +481,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -577,11 +569,6 @@ __device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t ta, uint32_t (&r)[16
       : "r"(ta)
       : "memory");
 }
-__device__ __forceinline__ void tmem_st_32x32b_x2(uint32_t ta, double d) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(ta), "r"((uint32_t)__double2loint(d)),
-               "r"((uint32_t)__double2hiint(d))
-               : "memory");
-}
 // 16 doubles -> column pairs 0..15 of the thread's lane: one asm block, so the base
 // address goes to a uniform register once (separate statements each get their own
 // R2UR) and every double stays in its own aligned register pair (no marshalling)
@@ -606,9 +593,6 @@ __device__ __forceinline__ void tmem_park16(uint32_t ta, const double (&v)[16]) 
       ::"r"(ta), "r"((uint32_t)__double2loint(v[0])), "r"((uint32_t)__double2hiint(v[0])), "r"((uint32_t)__double2loint(v[1])), "r"((uint32_t)__double2hiint(v[1])), "r"((uint32_t)__double2loint(v[2])), "r"((uint32_t)__double2hiint(v[2])), "r"((uint32_t)__double2loint(v[3])), "r"((uint32_t)__double2hiint(v[3])), "r"((uint32_t)__double2loint(v[4])), "r"((uint32_t)__double2hiint(v[4])), "r"((uint32_t)__double2loint(v[5])), "r"((uint32_t)__double2hiint(v[5])), "r"((uint32_t)__double2loint(v[6])), "r"((uint32_t)__double2hiint(v[6])), "r"((uint32_t)__double2loint(v[7])), "r"((uint32_t)__double2hiint(v[7])), "r"((uint32_t)__double2loint(v[8])), "r"((uint32_t)__double2hiint(v[8])), "r"((uint32_t)__double2loint(v[9])), "r"((uint32_t)__double2hiint(v[9])), "r"((uint32_t)__double2loint(v[10])), "r"((uint32_t)__double2hiint(v[10])), "r"((uint32_t)__double2loint(v[11])), "r"((uint32_t)__double2hiint(v[11])), "r"((uint32_t)__double2loint(v[12])), "r"((uint32_t)__double2hiint(v[12])), "r"((uint32_t)__double2loint(v[13])), "r"((uint32_t)__double2hiint(v[13])), "r"((uint32_t)__double2loint(v[14])), "r"((uint32_t)__double2hiint(v[14])), "r"((uint32_t)__double2loint(v[15])), "r"((uint32_t)__double2hiint(v[15]))
       : "memory");
 }
-__device__ __forceinline__ void tmem_ld_32x32b_x2(uint32_t ta, uint32_t& lo, uint32_t& hi) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(ta) : "memory");
-}
 #undef ISF_R8
 #undef ISF_W8
 // 16 doubles parked at columns 0..31 of the thread's lane -> registers (waits)
@@ -618,15 +602,6 @@ __device__ __forceinline__ void tmem_load16(uint32_t ta, double (&c)[16]) {
   tmem_wait_ld();
 #pragma unroll
   for (int i = 0; i < 16; ++i) c[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
-}
-__device__ __forceinline__ void tmem_store16(uint32_t ta, const double (&c)[16]) {
-  uint32_t r[32];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    r[2 * i] = (uint32_t)__double2loint(c[i]);
-    r[2 * i + 1] = (uint32_t)__double2hiint(c[i]);
-  }
-  tmem_st_32x32b_x32(ta, r);
 }
 
 // ---------------------------------------------------------------------------

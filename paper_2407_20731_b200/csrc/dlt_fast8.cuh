@@ -2,17 +2,20 @@
 //
 // One warp processes one (element, component) block of 8^3 fp64 values at a time;
 // warps take blocks round-robin (block = gw, gw + W, ...), so there is no
-// inter-warp dependency inside the hot kernels.  Per warp a ring of 4 KiB
-// shared-memory stages is filled by the TMA engine (cp.async.bulk issued by one
-// lane, mbarrier completion) kF8Stages blocks ahead.
+// inter-warp dependency inside the hot kernels.  Per warp a ring of shared-memory
+// stages is filled by the TMA engine (cp.async.bulk issued by one lane, mbarrier
+// completion) blocks ahead.
 //
 // Register layouts (lane l, 16 values per lane):
 //   z-lines : lane = (y = l>>2, q = l&3) holds x = 2q, 2q+1 at row y for all z
-//   y-lines : lane = (kz = l>>2, q = l&3) holds x = 2q, 2q+1 for all y at plane kz
+//   y-lines : compress lane = (q = l>>3, kz = l&7); decompress lane = (kz = l>>2, q = l&3)
+//             both hold x = 2q, 2q+1 for all y at plane kz
 //   x-lines : lane = (kz = l>>2, p = l&3) holds ky = 2p, 2p+1 for all x at plane kz
 // so after the forward x sweep lane l owns coefficients 16 l .. 16 l + 15.
-// The two role changes are in-place shared-memory transpositions with the XOR
-// swizzle swz() on 16-byte chunks, bank-conflict free for all four access patterns.
+// Compress: z -> y through the stage (padded 33-chunk planes), y -> x through TMEM
+// (tcgen05 16x256b, a two-bit lane/register exchange).  Decompress: both re-layouts
+// through the stage with the padded address kz * 36 + 4 ky + ky / 2 + xq.  All
+// access patterns are bank-conflict free with immediate offsets.
 // Forward sweeps z, y, x; inverse x, y, z (the pinned order of oracle/isf_oracle.c).
 #pragma once
 #include "dlt_kernels.cuh"
@@ -40,8 +43,6 @@ constexpr int kF8Stages = 2;   // TMA ring depth per warp (decompress)
 #endif
 constexpr int kC8Stages = ISF_C8_STAGES;  // TMA ring depth per warp (compress)
 
-// 16-byte chunk c (0..31) of plane kz (512 B)
-__device__ __forceinline__ int swz(int kz, int c) { return c ^ (((c >> 3) & 3) | ((kz & 1) << 2)); }
 
 // warp sum of per-lane values < 2^58 via three 32-bit REDUX.SUM (exact)
 __device__ __forceinline__ uint64_t warp_sum_u58(uint64_t x) {
@@ -382,19 +383,10 @@ struct Sel16 {
 __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t eps_q, unsigned long long* hist,
                                           uint32_t tpark) {
   Sel16 s{0u, 0ull, 0ull, 0, false};
-#ifdef ISF_OPT_DMAX
-  // max |a| by fp64 max (NaN-ignoring); a non-finite input makes every coefficient of
-  // the lx=8 block non-finite (no zero in F), so the lane maximum is Inf or NaN then
-  double am = fmax(fabs(v[0]), fabs(v[1]));
-#pragma unroll
-  for (int r = 2; r < 16; ++r) am = fmax(am, fabs(v[r]));
-  uint32_t hm = __reduce_max_sync(0xffffffffu, (uint32_t)__double2hiint(am));
-#else
   uint32_t hm = 0;
 #pragma unroll
   for (int r = 0; r < 16; ++r) hm = ::max(hm, (uint32_t)__double2hiint(v[r]) & 0x7fffffffu);
   hm = __reduce_max_sync(0xffffffffu, hm);
-#endif
   if (hm >= 0x7ff00000u) { s.nonfinite = true; return s; }
   int sexp;
   if (hm >= 0x00100000u) {
@@ -425,13 +417,8 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
 #pragma unroll
   for (int r = 0; r < 16; r += 2) {
     const double xa = __dmul_rn(v[r], f), xb = __dmul_rn(v[r + 1], f);
-#ifdef ISF_OPT_FMARD
-    t[r] = __fma_rd(xa, xa, 4503599627370496.0);
-    t[r + 1] = __fma_rd(xb, xb, 4503599627370496.0);
-#else
     t[r] = __dadd_rd(__dmul_rn(xa, xa), 4503599627370496.0);
     t[r + 1] = __dadd_rd(__dmul_rn(xb, xb), 4503599627370496.0);
-#endif
     t0 += (uint64_t)__double_as_longlong(t[r]);
     t1 += (uint64_t)__double_as_longlong(t[r + 1]);
   }
@@ -443,22 +430,11 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   const double tthr = __longlong_as_double((long long)(C52 + (thr < (1ull << 51) ? thr : (1ull << 51))));
   uint32_t mH = 0;
   uint64_t h0 = 0, h1s = 0;
-#if defined(ISF_OPT_HINT)
-  // integer classification (keeps the FP64 pipe free): t >= tthr <=> bits(t) >= bits(tthr)
-  const uint64_t tthr_b = C52 + (thr < (1ull << 51) ? thr : (1ull << 51));
-#pragma unroll
-  for (int r = 0; r < 16; r += 2) {
-    const uint64_t ba = (uint64_t)__double_as_longlong(t[r]), bb = (uint64_t)__double_as_longlong(t[r + 1]);
-    if (ba >= tthr_b) { mH |= 1u << r; h0 += ba; }
-    if (bb >= tthr_b) { mH |= 1u << (r + 1); h1s += bb; }
-  }
-#else
 #pragma unroll
   for (int r = 0; r < 16; r += 2) {
     if (t[r] >= tthr) { mH |= 1u << r; h0 += (uint64_t)__double_as_longlong(t[r]); }
     if (t[r + 1] >= tthr) { mH |= 1u << (r + 1); h1s += (uint64_t)__double_as_longlong(t[r + 1]); }
   }
-#endif
   const uint32_t nH = (uint32_t)__popc(mH);
   const uint64_t SH = warp_sum_u58(h0 + h1s - nH * C52);  // sum of lo over H
   const uint32_t NH = __reduce_add_sync(0xffffffffu, nH);
@@ -562,7 +538,7 @@ constexpr int kC8Smem = kC8Warps * kC8WarpBytes;
 // TMEM columns per warp: [0, 32) y->x re-layout buffer, then the parked coefficients
 // (one 32-column slot; three for the single-pass kernel, whose value writes trail the
 // selection by two rounds); the four warps of a lane quadrant (warp % 4) sit side by side.
-constexpr uint32_t pow2_ceil(uint32_t v) { return v <= 32u ? 32u : 2u * pow2_ceil((v + 1u) / 2u); }
+__host__ __device__ constexpr uint32_t pow2_ceil(uint32_t v) { return v <= 32u ? 32u : 2u * pow2_ceil((v + 1u) / 2u); }
 template <bool SP>
 __host__ __device__ constexpr uint32_t c8_tmem_cols() { return pow2_ceil((SP ? 128u : 64u) * (kC8Warps / 4)); }
 static_assert(kC8Warps % 4 == 0 && c8_tmem_cols<true>() <= 512, "TMEM budget");
@@ -746,7 +722,6 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     // role; its double (g, j, h) of instruction g, rep j, half h holds
     // x2 = g, x1 = h, ky0 = j1, x0 = j0.
     {
-#ifndef ISF_T2_X2
       uint32_t r[32];
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
@@ -755,13 +730,6 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
         r[2 * c + 1] = (uint32_t)__double2hiint(v[2 * ky + x0]);
       }
       tmem_st_32x32b_x32(tx, r);
-#else
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const int ky = ((c >> 1) & 1) * 4 + (c & 1) * 2 + (c >> 3), x0 = (c >> 2) & 1;
-        tmem_st_32x32b_x2(tx + 2u * c, v[2 * ky + x0]);
-      }
-#endif
       tmem_wait_st();
       uint32_t a0[16], a1[16];
       tmem_ld_16x256b_x4(tx, a0);
