@@ -598,12 +598,13 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   pdl_wait();  // the field / stream / workspace may come from the previous kernel
   pdl_launch_dependents();
   const uint32_t tx = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (SP ? 128u : 64u) * (uint32_t)(warp >> 2);
+  const uint32_t wbase_a = smem_u32(wbase), bars_a = smem_u32(bars);  // hoisted shared-window addresses
   const uint64_t pol_stream = l2_policy_evict_first();  // the field is read once
   const uint64_t pol_keep = l2_policy_evict_last();     // value slots: re-read by compact8_kernel
   auto issue = [&](uint64_t blk, int st) {
     if (lane == 0 && blk < B) {
-      mbar_arrive_tx(&bars[st], 4096u);
-      bulk_g2s_hint(wbase + st * kC8Stage, A.field + blk * 512, 4096u, &bars[st], pol_stream);
+      mbar_arrive_tx_a(bars_a + 8u * st, 4096u);
+      bulk_g2s_hint_a(wbase_a + (uint32_t)(st * kC8Stage), A.field + blk * 512, 4096u, bars_a + 8u * st, pol_stream);
     }
   };
 #pragma unroll
@@ -683,7 +684,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     uint32_t mask = 0, kept = 0;
     if (!SP || blk < B) {  // warp-uniform
     double2* sb = reinterpret_cast<double2*>(wbase + st * kC8Stage);
-    mbar_wait(&bars[st], (ph >> st) & 1u);
+    mbar_wait_a(bars_a + 8u * st, (ph >> st) & 1u);
     ph ^= 1u << st;
     double v[16];
     // z-lines: lane = (y = l/4, q = l%4) holds x = 2q, 2q+1 of row y for all z
