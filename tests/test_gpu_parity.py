@@ -387,3 +387,37 @@ def test_single_pass_schedule(native, oracle, kind):
         plan.set_compress_mode(PK.LossyPlan.TWO_PASS)
     with pytest.raises(PK.IsfError):
         plan.set_compress_mode(7)
+
+
+@pytest.mark.parametrize("P,mode", [(8, 0), (8, 1), (6, 0), (12, 0)])
+def test_status_flags_all_schedules(native, oracle, P, mode):
+    """Non-finite input and a stream capacity that cannot hold the kept values raise
+    the same status bits on every compress schedule (two-pass lx=8, single-pass lx=8,
+    generic slots + compact_generic), and a good call afterwards is clean again."""
+    import paper_2407_20731_b200 as PK
+    plan = PK.LossyPlan(P, 1, 0)
+    plan.set_compress_mode(mode) if P == 8 else None
+    n_el = 3000
+    u = oracle.gen_spectral(P, n_el)
+    x = torch.from_numpy(u).cuda()
+    stats = torch.zeros(12, dtype=torch.float64, device="cuda")
+    hdr = plan.header_bytes(n_el)
+    # 1. capacity: header plus room for 10 values only (the spectrum keeps far more)
+    small = torch.zeros(hdr + 80, dtype=torch.uint8, device="cuda")
+    plan.compress_async(x, n_el, 1e-5, small, stats)
+    torch.cuda.synchronize()
+    assert int(stats.view(torch.int64)[10].item()) & 4, "overflow not flagged"
+    # 2. non-finite input
+    bad = x.clone()
+    bad[777] = float("nan")
+    st = torch.zeros(plan.capacity(n_el), dtype=torch.uint8, device="cuda")
+    plan.compress_async(bad, n_el, 1e-3, st, stats)
+    torch.cuda.synchronize()
+    assert int(stats.view(torch.int64)[10].item()) & 1, "non-finite not flagged"
+    # 3. a good call right after: clean status, oracle-identical stream
+    plan.compress_async(x, n_el, 1e-3, st, stats)
+    torch.cuda.synchronize()
+    si = stats.view(torch.int64)
+    assert int(si[10].item()) == 0
+    rc, ref, _ = oracle.compress(u, P, 1, 1e-3)
+    assert np.array_equal(st[: int(si[8].item())].cpu().numpy(), ref)
