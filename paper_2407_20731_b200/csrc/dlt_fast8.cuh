@@ -1286,35 +1286,44 @@ __global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decom
       lines8<0, 1, 0, 8, 2, true>(v);
     }
     double2* sb = reinterpret_cast<double2*>(sp);
+    // Rows that are all zero and never read again are not moved: with Ky < 16 the
+    // y-lines only read ky < 4, with Kz < 16 the z-lines only read planes kz < 4, so
+    // lanes of planes kz >= 4 skip their stores and loads (their sweeps run on stale
+    // registers whose results are dropped) -- fewer shared-memory wavefronts.
+    const bool lowz = Kz < 16u;
+    const bool zlive = !lowz || kzp < 4;
 #pragma unroll
     for (int kyi = 0; kyi < 2; ++kyi)
 #pragma unroll
       for (int qq = 0; qq < 4; ++qq)
-        sb[xoff + 4 * kyi + qq] = make_double2(v[kyi * 8 + 2 * qq], v[kyi * 8 + 2 * qq + 1]);
+        if (zlive && (Ky >= 16u || 2 * qp + kyi < 4))
+          sb[xoff + 4 * kyi + qq] = make_double2(v[kyi * 8 + 2 * qq], v[kyi * 8 + 2 * qq + 1]);
     __syncwarp();
     if (Ky < 16u) {
 #pragma unroll
-      for (int ky = 0; ky < 4; ++ky) {
-        const double2 t = sb[yoff + 4 * ky + (ky >> 1)];
-        v[2 * ky] = t.x;
-        v[2 * ky + 1] = t.y;
-      }
+      for (int ky = 0; ky < 4; ++ky)
+        if (zlive) {
+          const double2 t = sb[yoff + 4 * ky + (ky >> 1)];
+          v[2 * ky] = t.x;
+          v[2 * ky + 1] = t.y;
+        }
       __syncwarp();
       inv2_low8<2, 0, 1, 1>(v);
     } else {
 #pragma unroll
-      for (int ky = 0; ky < 8; ++ky) {
-        const double2 t = sb[yoff + 4 * ky + (ky >> 1)];
-        v[2 * ky] = t.x;
-        v[2 * ky + 1] = t.y;
-      }
+      for (int ky = 0; ky < 8; ++ky)
+        if (zlive) {
+          const double2 t = sb[yoff + 4 * ky + (ky >> 1)];
+          v[2 * ky] = t.x;
+          v[2 * ky + 1] = t.y;
+        }
       __syncwarp();
       lines8<1, 2, 0, 1, 2, true>(v);
     }
 #pragma unroll
-    for (int yy = 0; yy < 8; ++yy) sb[yoff + 4 * yy + (yy >> 1)] = make_double2(v[2 * yy], v[2 * yy + 1]);
+    for (int yy = 0; yy < 8; ++yy)
+      if (zlive) sb[yoff + 4 * yy + (yy >> 1)] = make_double2(v[2 * yy], v[2 * yy + 1]);
     __syncwarp();
-    const bool lowz = Kz < 16u;
 #pragma unroll
     for (int z = 0; z < 8; ++z)
       if (z < 4 || !lowz) {
