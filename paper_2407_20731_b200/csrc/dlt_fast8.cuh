@@ -1135,6 +1135,18 @@ __global__ void __launch_bounds__(kCompactThreads, 2) compact8_kernel(uint8_t* s
 // nothing but the sign of zero: every intermediate keeps the real value of the
 // dense chain, sweep after sweep, and the +0 canonicalisation of the reconstruction
 // (applied by the oracle too) makes the bits identical.
+// One line of inv2_low8 (same chains).
+template <int S, int O, int T, int N>
+__device__ __forceinline__ void inv1_low8(double (&v)[N]) {
+  const double a[4] = {v[O], v[O + S], v[O + 2 * S], v[O + 3 * S]};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double e = __fma_rn(Bm<8, T>(i, 2), a[2], __fma_rn(Bm<8, T>(i, 0), a[0], 0.0));
+    const double d = __fma_rn(Bm<8, T>(i, 3), a[3], __fma_rn(Bm<8, T>(i, 1), a[1], 0.0));
+    v[O + i * S] = __dadd_rn(e, d);
+    v[O + (7 - i) * S] = __dsub_rn(e, d);
+  }
+}
 template <int S, int O0, int O1, int T, int N>
 __device__ __forceinline__ void inv2_low8(double (&v)[N]) {
   const double a0[4] = {v[O0], v[O0 + S], v[O0 + 2 * S], v[O0 + 3 * S]};
@@ -1261,6 +1273,51 @@ __global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decom
       __syncwarp();
     }
     double v[16];
+    const bool lowz = Kz < 16u;
+    if (!ERR && (Kx | Ky | Kz) < 16u) {  // (the error-report instantiation keeps the
+      // general path: the extra live state would spill)
+      // Low cube (the common smooth case): every kept coefficient has kx, ky, kz < 4.
+      // The inverse then runs on 16 x-lines, 32 y-lines and 64 z-lines instead of 64
+      // each, one line per lane for x and y (the same pinned chains as inv2_low8),
+      // with two small padded shared-memory re-layouts (stride 9 doubles).
+      double* fx = reinterpret_cast<double*>(sp);  // [16 x-lines (kz, ky)][9]
+      double* fy = fx + 16 * 9;                    // [32 y-lines (kz, x)][9]
+      {
+        const int L = lane & 15, lky = L & 3;
+        const int ml = 4 * (L >> 2) + (lky >> 1);  // mask lane of the line (kz, ky)
+        const uint32_t mw = __shfl_sync(0xffffffffu, m, ml);
+        const uint32_t bse = __shfl_sync(0xffffffffu, inoff, ml);
+        const uint32_t lb = (lky & 1) ? 8u : 0u;
+        double a8[8];
+#pragma unroll
+        for (int kx = 0; kx < 4; ++kx) {
+          const uint32_t bit = lb + kx;
+          a8[kx] = ((mw >> bit) & 1u) ? sv0[bse + __popc(mw & ((1u << bit) - 1u))] : 0.0;
+        }
+        inv1_low8<1, 0, 0>(a8);  // inverse x sweep
+        __syncwarp();            // the values region is read: reuse the stage
+        if (lane < 16) {
+#pragma unroll
+          for (int x = 0; x < 8; ++x) fx[L * 9 + x] = a8[x];
+        }
+      }
+      __syncwarp();
+      {
+        const int ykz = lane >> 3, yx = lane & 7;
+        double b8[8];
+#pragma unroll
+        for (int ky = 0; ky < 4; ++ky) b8[ky] = fx[(4 * ykz + ky) * 9 + yx];
+        inv1_low8<1, 0, 1>(b8);  // inverse y sweep
+#pragma unroll
+        for (int yy = 0; yy < 8; ++yy) fy[(8 * ykz + yx) * 9 + yy] = b8[yy];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int z = 0; z < 4; ++z) {
+        v[2 * z] = fy[(8 * z + 2 * q) * 9 + y];
+        v[2 * z + 1] = fy[(8 * z + 2 * q + 1) * 9 + y];
+      }
+    } else {
     const double* sv = sv0 + inoff;
     if (Kx < 16u) {  // warp-uniform: only kx 0..3 occupied
       int o = 0;  // running value index (bits 4..7 and 12..15 are clear here)
@@ -1290,7 +1347,6 @@ __global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decom
     // y-lines only read ky < 4, with Kz < 16 the z-lines only read planes kz < 4, so
     // lanes of planes kz >= 4 skip their stores and loads (their sweeps run on stale
     // registers whose results are dropped) -- fewer shared-memory wavefronts.
-    const bool lowz = Kz < 16u;
     const bool zlive = !lowz || kzp < 4;
 #pragma unroll
     for (int kyi = 0; kyi < 2; ++kyi)
@@ -1331,6 +1387,7 @@ __global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decom
         v[2 * z] = t.x;
         v[2 * z + 1] = t.y;
       }
+    }
     fence_proxy_async();
     __syncwarp();
     issue(blk + 2 * W, st, r0, r1);
