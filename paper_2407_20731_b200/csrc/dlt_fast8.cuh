@@ -796,8 +796,15 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       }
     }
     if (!sel.nonfinite && sel.T) {
-      tot_acc += scale2((double)sel.T, -2 * sel.k);
-      disc_acc += scale2((double)sel.hdisc, -2 * sel.k);
+      const int e2 = -2 * sel.k;
+      if (e2 >= -1022 && e2 <= 1023) {  // the usual case: one exact power-of-two scale
+        const double sc = pow2d(e2);
+        tot_acc = __fma_rn((double)sel.T, sc, tot_acc);
+        disc_acc = __fma_rn((double)sel.hdisc, sc, disc_acc);
+      } else {
+        tot_acc += ldexp((double)sel.T, e2);
+        disc_acc += ldexp((double)sel.hdisc, e2);
+      }
     }
     (void)off;
     }  // live block
