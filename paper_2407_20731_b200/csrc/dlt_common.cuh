@@ -450,10 +450,10 @@ __device__ void radix_select_w(const LaneGroup<G>& g, const Src& src, const Wt& 
 }
 
 // element sources for radix_select
-struct SrcCompacted {  // candidate keys + indices (generic kernels)
-  const uint64_t* keys;
+struct SrcIndirect {  // candidate indices into the block's coefficients (generic kernels)
+  const double* a;
   const uint16_t* idxs;
-  __device__ __forceinline__ void operator()(int p, uint64_t& k, uint32_t& ix) const { k = keys[p]; ix = idxs[p]; }
+  __device__ __forceinline__ void operator()(int p, uint64_t& k, uint32_t& ix) const { ix = idxs[p]; k = abs_bits(a[ix]); }
 };
 struct SrcDense {  // raw coefficients in natural order, index = position (fast kernels)
   const double* a;

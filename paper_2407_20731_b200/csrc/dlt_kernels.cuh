@@ -88,24 +88,50 @@ __device__ __forceinline__ uint32_t claim_tile(uint32_t* counter) {
 }
 
 // --------------------------- generic (any lx, comps) ------------------------
-constexpr int kGenThreads = 128;
+#ifndef ISF_GEN_CTHREADS
+#define ISF_GEN_CTHREADS 32
+#endif
+// compress_generic: one warp per block (selection is one warp's job, so wider CTAs idle)
+constexpr int kGenCThreads = ISF_GEN_CTHREADS;
+// decompress_generic CTA width per lx (measured on the cfg4 sweep, profiles/r1_summary.md):
+// small blocks want more CTAs, large ones more threads per block
+template <int LX>
+__host__ __device__ constexpr int gen_dthreads() {
+#ifdef ISF_GEN_DTHREADS
+  return ISF_GEN_DTHREADS;
+#else
+  return LX <= 7 ? 64 : LX <= 11 ? 128 : 256;
+#endif
+}
 
 template <int LX>
 struct GenSmem {
   static constexpr int N3 = LX * LX * LX;
   static constexpr int W = (N3 + 63) / 64;
   static constexpr size_t u_off = 0;
-  static constexpr size_t key_off = u_off + sizeof(double) * N3;
-  static constexpr size_t idx_off = key_off + sizeof(uint64_t) * N3;
+  static constexpr size_t idx_off = u_off + sizeof(double) * N3;
   static constexpr size_t hist_off = ((idx_off + sizeof(uint16_t) * N3) + 15) & ~size_t(15);
   static constexpr size_t mask_off = hist_off + 64 * 8;
   static constexpr size_t misc_off = mask_off + 64 * 8;
   static constexpr size_t bytes = misc_off + 64;
 };
 
+// decompress_generic: the block, per-word prefix popcounts, mask words, misc and the
+// per-warp error partials (no selection scratch, so more resident CTAs)
+template <int LX>
+struct GenDSmem {
+  static constexpr int N3 = LX * LX * LX;
+  static constexpr size_t u_off = 0;
+  static constexpr size_t wpre_off = sizeof(double) * N3;
+  static constexpr size_t mask_off = wpre_off + 64 * 4;
+  static constexpr size_t misc_off = mask_off + 64 * 8;
+  static constexpr size_t red_off = misc_off + 64;
+  static constexpr size_t bytes = red_off + (gen_dthreads<LX>() / 32) * 4 * 8;
+};
+
 // selection on warp 0 over the coefficients in smem u[]
 template <int LX>
-__device__ void select_generic(double* u, uint64_t eps_q, uint64_t* ckeys, uint16_t* cidx,
+__device__ void select_generic(double* u, uint64_t eps_q, uint16_t* cidx,
                                unsigned long long* hist, uint64_t* maskw, uint64_t& T_out,
                                uint64_t& hdisc_out, int& k_out, bool& nonfinite) {
   constexpr int N3 = LX * LX * LX;
@@ -164,18 +190,14 @@ __device__ void select_generic(double* u, uint64_t eps_q, uint64_t* ckeys, uint1
         if (h <= thr) { if (h <= thrn) SL += h; else cand = true; }
       }
       const unsigned b = __ballot_sync(0xffffffffu, cand);
-      if (cand) {
-        const uint32_t o = base + __popc(b & ((1u << lane) - 1u));
-        ckeys[o] = abs_bits(u[p]);
-        cidx[o] = (uint16_t)p;
-      }
+      if (cand) cidx[base + __popc(b & ((1u << lane) - 1u))] = (uint16_t)p;
       base += __popc(b);
     }
     SL = g.sum(SL);
     __syncwarp();
     uint64_t tstar, dsum;
     uint32_t icut;
-    radix_select<32>(g, SrcCompacted{ckeys, cidx}, (int)base, thr - SL, f, hist, tstar, icut, dsum);
+    radix_select<32>(g, SrcIndirect{u, cidx}, (int)base, thr - SL, f, hist, tstar, icut, dsum);
     for (int r = 0; r < NR; ++r) {
       const int p = r * 32 + lane;
       bool kept = false;
@@ -255,13 +277,12 @@ __device__ void select_linf(const double* u, double umax, double eps, unsigned l
 }
 
 template <int LX>
-__global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) {
+__global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A) {
   constexpr int N = LX, N2 = LX * LX, N3 = LX * LX * LX;
   constexpr int W = (N3 + 63) / 64;
   using L = GenSmem<LX>;
   extern __shared__ __align__(128) unsigned char smem[];
   double* u = reinterpret_cast<double*>(smem + L::u_off);
-  uint64_t* ckeys = reinterpret_cast<uint64_t*>(smem + L::key_off);
   uint16_t* cidx = reinterpret_cast<uint16_t*>(smem + L::idx_off);
   unsigned long long* hist = reinterpret_cast<unsigned long long*>(smem + L::hist_off);
   uint64_t* maskw = reinterpret_cast<uint64_t*>(smem + L::mask_off);
@@ -283,7 +304,7 @@ __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) 
     const uint64_t e = blk / A.comps, c = blk % A.comps;
     const double* src = A.field + e * (uint64_t)N3 * A.comps + c;
     uint64_t um = 0;
-    for (int p = tid; p < N3; p += kGenThreads) {
+    for (int p = tid; p < N3; p += kGenCThreads) {
       const double x = src[(uint64_t)p * A.comps];
       u[p] = x;
       const uint64_t b = abs_bits(x);
@@ -295,11 +316,11 @@ __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) 
       atomicMax(reinterpret_cast<unsigned long long*>(&misc[3]), (unsigned long long)um);
     }
     __syncthreads();
-    for (int l = tid; l < N2; l += kGenThreads) fwd_line_ptr<LX>(u + l, N2);                       // z
+    for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + l, N2);                       // z
     __syncthreads();
-    for (int l = tid; l < N2; l += kGenThreads) fwd_line_ptr<LX>(u + (l / N) * N2 + (l % N), N);  // y
+    for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + (l / N) * N2 + (l % N), N);  // y
     __syncthreads();
-    for (int l = tid; l < N2; l += kGenThreads) fwd_line_ptr<LX>(u + l * N, 1);                     // x
+    for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + l * N, 1);                     // x
     __syncthreads();
     if (warp == 0) {
       uint64_t T, hd;
@@ -310,7 +331,7 @@ __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) 
         T = hd = 0;
         k = 0;
       } else {
-        select_generic<LX>(u, A.eps_q, ckeys, cidx, hist, maskw, T, hd, k, nf);
+        select_generic<LX>(u, A.eps_q, cidx, hist, maskw, T, hd, k, nf);
       }
       if (nf) {
         for (int w = lane; w < W; w += 32) maskw[w] = 0ull;
@@ -343,12 +364,12 @@ __global__ void __launch_bounds__(kGenThreads) compress_generic(CompressArgs A) 
     __syncthreads();
     if (A.vslot) {
       double* slot = A.vslot + blk * (uint64_t)N3;
-      for (int p = tid; p < N3; p += kGenThreads)
+      for (int p = tid; p < N3; p += kGenCThreads)
         if ((maskw[p >> 6] >> (p & 63)) & 1ull) slot[p] = u[p];
     } else if (misc[2]) {
       // kept values in ascending index: rank = popcount of lower mask bits
       const uint64_t prefix = misc[1];
-      for (int p = tid; p < N3; p += kGenThreads) {
+      for (int p = tid; p < N3; p += kGenCThreads) {
         const uint64_t mw = maskw[p >> 6];
         if ((mw >> (p & 63)) & 1ull) {
           uint32_t rank = (uint32_t)__popcll(mw & ((1ull << (p & 63)) - 1ull));
@@ -391,16 +412,17 @@ __global__ void __launch_bounds__(256) compact_generic_kernel(const uint8_t* str
 }
 
 template <int LX>
-__global__ void __launch_bounds__(kGenThreads) decompress_generic(DecompressArgs A) {
+__global__ void __launch_bounds__(gen_dthreads<LX>()) decompress_generic(DecompressArgs A) {
   constexpr int N = LX, N2 = LX * LX, N3 = LX * LX * LX;
+  constexpr int kT = gen_dthreads<LX>();
   constexpr int W = (N3 + 63) / 64;
-  using L = GenSmem<LX>;
+  using L = GenDSmem<LX>;
   extern __shared__ __align__(128) unsigned char smem[];
   double* u = reinterpret_cast<double*>(smem + L::u_off);
   uint64_t* maskw = reinterpret_cast<uint64_t*>(smem + L::mask_off);
-  uint32_t* wpre = reinterpret_cast<uint32_t*>(smem + L::key_off);  // prefix popcounts per word
+  uint32_t* wpre = reinterpret_cast<uint32_t*>(smem + L::wpre_off);  // prefix popcounts per word
   uint64_t* misc = reinterpret_cast<uint64_t*>(smem + L::misc_off);
-  double* red = reinterpret_cast<double*>(smem + L::hist_off);     // 4 warps x 4
+  double* red = reinterpret_cast<double*>(smem + L::red_off);        // warps x 4
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t* counts = reinterpret_cast<const uint32_t*>(A.stream);
   const uint64_t* masks = reinterpret_cast<const uint64_t*>(A.stream + A.mask_off);
@@ -444,7 +466,7 @@ __global__ void __launch_bounds__(kGenThreads) decompress_generic(DecompressArgs
     __syncthreads();
     const uint64_t prefix = misc[1];
     const bool bad = misc[2] != 0;
-    for (int p = tid; p < N3; p += kGenThreads) {
+    for (int p = tid; p < N3; p += kT) {
       const uint64_t mw = maskw[p >> 6];
       double val = 0.0;
       if (!bad && ((mw >> (p & 63)) & 1ull))
@@ -452,16 +474,16 @@ __global__ void __launch_bounds__(kGenThreads) decompress_generic(DecompressArgs
       u[p] = val;
     }
     __syncthreads();
-    for (int l = tid; l < N2; l += kGenThreads) inv_line_ptr<LX>(u + l * N, 1);                     // x
+    for (int l = tid; l < N2; l += kT) inv_line_ptr<LX>(u + l * N, 1);                     // x
     __syncthreads();
-    for (int l = tid; l < N2; l += kGenThreads) inv_line_ptr<LX>(u + (l / N) * N2 + (l % N), N);  // y
+    for (int l = tid; l < N2; l += kT) inv_line_ptr<LX>(u + (l / N) * N2 + (l % N), N);  // y
     __syncthreads();
-    for (int l = tid; l < N2; l += kGenThreads) inv_line_ptr<LX>(u + l, N2);                       // z
+    for (int l = tid; l < N2; l += kT) inv_line_ptr<LX>(u + l, N2);                       // z
     __syncthreads();
     const uint64_t e = blk / A.comps, c = blk % A.comps;
     double* dst = A.out + e * (uint64_t)N3 * A.comps + c;
     const double* org = A.orig ? A.orig + e * (uint64_t)N3 * A.comps + c : nullptr;
-    for (int p = tid; p < N3; p += kGenThreads) {
+    for (int p = tid; p < N3; p += kT) {
       const double val = __dadd_rn(u[p], 0.0);  // zero results are written as +0
       dst[(uint64_t)p * A.comps] = val;
       if (org) {
@@ -494,7 +516,7 @@ __global__ void __launch_bounds__(kGenThreads) decompress_generic(DecompressArgs
     if (tid == 0) {
       double se = 0, sn = 0;
       uint64_t me = 0, mu = 0;
-      for (int w = 0; w < kGenThreads / 32; ++w) {
+      for (int w = 0; w < kT / 32; ++w) {
         se = __dadd_rn(se, red[w * 4]); sn = __dadd_rn(sn, red[w * 4 + 1]);
         uint64_t t = (uint64_t)__double_as_longlong(red[w * 4 + 2]); me = t > me ? t : me;
         t = (uint64_t)__double_as_longlong(red[w * 4 + 3]); mu = t > mu ? t : mu;

@@ -218,35 +218,33 @@ int launch_compress_generic(isf_lossy_plan* p, CompressArgs a, cudaStream_t s) {
   static bool attr_set[64] = {};
   if (!attr_set[p->device]) {
     CUDA_TRY(cudaFuncSetAttribute(compress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CUDA_TRY(cudaFuncSetAttribute(decompress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr_set[p->device] = true;
   }
   int occ = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress_generic<LX>, kGenThreads, sm));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress_generic<LX>, kGenCThreads, sm));
   occ = std::max(occ, 1);
   const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->sms * occ, a.ws.ntiles ? a.ws.ntiles : 1);
   a.ws.total_warps = grid;
-  compress_generic<LX><<<grid, kGenThreads, sm, s>>>(a);
+  compress_generic<LX><<<grid, kGenCThreads, sm, s>>>(a);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
 
 template <int LX>
 int launch_decompress_generic(isf_lossy_plan* p, DecompressArgs a, cudaStream_t s, uint32_t* grid_out) {
-  const size_t sm = GenSmem<LX>::bytes;
+  const size_t sm = GenDSmem<LX>::bytes;
   static bool attr_set[64] = {};
   if (!attr_set[p->device]) {
-    CUDA_TRY(cudaFuncSetAttribute(compress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CUDA_TRY(cudaFuncSetAttribute(decompress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr_set[p->device] = true;
   }
   int occ = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress_generic<LX>, kGenThreads, sm));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress_generic<LX>, gen_dthreads<LX>(), sm));
   occ = std::max(occ, 1);
   const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->sms * occ, a.ws.ntiles ? a.ws.ntiles : 1);
   a.ws.total_warps = grid;
   *grid_out = grid;
-  decompress_generic<LX><<<grid, kGenThreads, sm, s>>>(a);
+  decompress_generic<LX><<<grid, gen_dthreads<LX>(), sm, s>>>(a);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
