@@ -167,47 +167,47 @@ __device__ void select_generic(double* u, uint64_t eps_q, uint16_t* cidx,
   T = g.sum(T);
   T_out = T;
   const uint64_t thr = __umul64hi(T, eps_q);
-  uint64_t SN = 0;
-  for (int p = lane; p < N3; p += 32) { const uint64_t h = e_hi(u[p], f); if (h <= thr) SN += h; }
+  // one pass: the sure-kept mask (e > thr), the discardable sum SN, and, in case SN
+  // exceeds the budget, the sure-discarded sum SL (e <= thr / N3) with the candidates
+  // in between compacted by index for the radix select
+  const uint64_t thrn = thr / (uint64_t)N3;
+  uint64_t SN = 0, SL = 0;
+  uint32_t base = 0;
+  for (int r = 0; r < NR; ++r) {
+    const int p = r * 32 + lane;
+    bool sure = false, cand = false;
+    if (p < N3) {
+      const uint64_t h = e_hi(u[p], f);
+      sure = h > thr;
+      if (!sure) {
+        SN += h;
+        if (h <= thrn) SL += h; else cand = true;
+      }
+    }
+    const unsigned bk = __ballot_sync(0xffffffffu, sure);
+    const unsigned bc = __ballot_sync(0xffffffffu, cand);
+    if (lane == 0) maskw[r >> 1] |= (uint64_t)bk << (32 * (r & 1));
+    if (cand) cidx[base + __popc(bc & ((1u << lane) - 1u))] = (uint16_t)p;
+    base += __popc(bc);
+  }
   SN = g.sum(SN);
   if (SN <= thr) {
-    for (int r = 0; r < NR; ++r) {
-      const int p = r * 32 + lane;
-      const bool kept = p < N3 && e_hi(u[p], f) > thr;
-      const unsigned b = __ballot_sync(0xffffffffu, kept);
-      if (lane == 0) maskw[r >> 1] |= (uint64_t)b << (32 * (r & 1));
-    }
     hdisc_out = SN;
   } else {
-    const uint64_t thrn = thr / (uint64_t)N3;
-    uint64_t SL = 0;
-    uint32_t base = 0;
-    for (int r = 0; r < NR; ++r) {
-      const int p = r * 32 + lane;
-      bool cand = false;
-      if (p < N3) {
-        const uint64_t h = e_hi(u[p], f);
-        if (h <= thr) { if (h <= thrn) SL += h; else cand = true; }
-      }
-      const unsigned b = __ballot_sync(0xffffffffu, cand);
-      if (cand) cidx[base + __popc(b & ((1u << lane) - 1u))] = (uint16_t)p;
-      base += __popc(b);
-    }
     SL = g.sum(SL);
     __syncwarp();
     uint64_t tstar, dsum;
     uint32_t icut;
     radix_select<32>(g, SrcIndirect{u, cidx}, (int)base, thr - SL, f, hist, tstar, icut, dsum);
+    // the cut (tstar, icut) is a candidate key (>= 1 candidate here, since SL <= thr < SN)
+    // and e_hi is monotone in |a|: sure-discarded coefficients lie strictly below it, sure-
+    // kept ones above, so the key comparison alone decides every coefficient
     for (int r = 0; r < NR; ++r) {
       const int p = r * 32 + lane;
       bool kept = false;
       if (p < N3) {
-        const uint64_t h = e_hi(u[p], f);
-        if (h > thr) kept = true;
-        else if (h > thrn) {
-          const uint64_t kk = abs_bits(u[p]);
-          kept = kk > tstar || (kk == tstar && (uint32_t)p < icut);
-        }
+        const uint64_t kk = abs_bits(u[p]);
+        kept = kk > tstar || (kk == tstar && (uint32_t)p < icut);
       }
       const unsigned b = __ballot_sync(0xffffffffu, kept);
       if (lane == 0) maskw[r >> 1] |= (uint64_t)b << (32 * (r & 1));

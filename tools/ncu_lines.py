@@ -26,8 +26,11 @@ def main(rep, kernel, so, blocks, top=40, mangled=None):
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=tmp, capture_output=True)
     cub = [l for l in os.listdir(tmp) if l.endswith(".cubin")]
-    dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub[0])], capture_output=True, text=True).stdout.split("\n")
     key = mangled or (str(len(kernel.split("<")[0])) + kernel.split("<")[0])
+    for c in cub:  # the cubin that holds the kernel
+        dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, c)], capture_output=True, text=True).stdout.split("\n")
+        if any(l.startswith(".text.") and key in l for l in dis):
+            break
     start = [i for i, l in enumerate(dis) if l.startswith(".text.") and key in l][0]
     fl, offmap = None, {}
     for l in dis[start + 1:]:
