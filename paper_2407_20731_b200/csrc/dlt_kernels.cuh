@@ -431,36 +431,35 @@ __global__ void __launch_bounds__(gen_dthreads<LX>()) decompress_generic(Decompr
   constexpr uint64_t lastmask = (N3 % 64) ? ((1ull << (N3 % 64)) - 1ull) : ~0ull;
   double e2 = 0.0, n2 = 0.0;
   uint64_t einf = 0, uinf = 0;
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) misc[0] = atomicAdd(A.ws.counter, 1u);
-    __syncthreads();
-    const uint32_t tile = (uint32_t)misc[0];
-    if (tile >= A.ws.ntiles) {
-      if (tid == 0 && tile == A.ws.ntiles + A.ws.total_warps - 1) *A.ws.counter = 0;
-      break;
-    }
-    const uint64_t blk = tile;
+  // static round-robin over the blocks (uniform cost; value offsets come from the
+  // block_offsets8_kernel scan, A.off, which the host always provides)
+  for (uint64_t blk = blockIdx.x; blk < A.ws.ntiles; blk += gridDim.x) {
+    __syncthreads();  // the previous block's smem is consumed
     if (warp == 0) {
       const uint32_t cnt = counts[blk];
-      uint32_t pc = 0;
-      for (int w = lane; w < W; w += 32) {
-        uint64_t mw = masks[blk * W + w];
-        if (w == W - 1 && (mw & ~lastmask)) { atomicOr(A.ws.flags, kFlagShape); mw &= lastmask; }
-        maskw[w] = mw;
-        pc += __popcll(mw);
+      // mask words lane and lane + 32 (W <= 64), per-word exclusive popcount prefix
+      uint64_t m0 = 0, m1 = 0;
+      if (lane < W) m0 = masks[blk * W + lane];
+      if (lane + 32 < W) m1 = masks[blk * W + lane + 32];
+      if (lane == W - 1 && (m0 & ~lastmask)) { atomicOr(A.ws.flags, kFlagShape); m0 &= lastmask; }
+      if (lane + 32 == W - 1 && (m1 & ~lastmask)) { atomicOr(A.ws.flags, kFlagShape); m1 &= lastmask; }
+      const uint32_t c0 = (uint32_t)__popcll(m0), c1 = (uint32_t)__popcll(m1);
+      uint32_t i0 = c0, i1 = c1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t0 = __shfl_up_sync(0xffffffffu, i0, o), t1 = __shfl_up_sync(0xffffffffu, i1, o);
+        if (lane >= o) { i0 += t0; i1 += t1; }
       }
-      const LaneGroup<32> g;
-      pc = g.sum(pc);
-      // offsets precomputed by block_offsets8_kernel (no serial look-back chain)
-      const uint64_t prefix = A.off ? A.off[blk] : warp_lookback(A.ws.status, tile, cnt, A.ws.epoch);
-      bool bad = pc != cnt || prefix + cnt > nvals_avail;
+      const uint32_t tot0 = __shfl_sync(0xffffffffu, i0, 31);
+      const uint32_t pc = tot0 + __shfl_sync(0xffffffffu, i1, 31);
+      if (lane < W) { maskw[lane] = m0; wpre[lane] = i0 - c0; }
+      if (lane + 32 < W) { maskw[lane + 32] = m1; wpre[lane + 32] = tot0 + i1 - c1; }
+      const uint64_t prefix = A.off[blk];
+      const bool bad = pc != cnt || prefix + cnt > nvals_avail;
       if (lane == 0) {
         if (bad) atomicOr(A.ws.flags, kFlagShape);
         misc[1] = prefix;
         misc[2] = bad;
-        uint32_t run = 0;
-        for (int w = 0; w < W; ++w) { wpre[w] = run; run += __popcll(maskw[w]); }
       }
     }
     __syncthreads();
