@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
     __syncthreads();
     for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + l * N, 1);                     // x
     __syncthreads();
-    if (warp == 0) {
+    if (kGenCThreads == 32 || warp == 0) {  // single-warp CTA: no divergent region
       uint64_t T, hd;
       int k;
       bool nf;
