@@ -290,7 +290,6 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* counts = reinterpret_cast<uint32_t*>(A.stream);
   uint64_t* masks = reinterpret_cast<uint64_t*>(A.stream + A.mask_off);
-  double* vals = reinterpret_cast<double*>(A.stream + A.val_off);
   for (;;) {
     __syncthreads();
     if (tid == 0) misc[0] = atomicAdd(A.ws.counter, 1u);
@@ -342,42 +341,21 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
       for (int w = lane; w < W; w += 32) nk += __popcll(maskw[w]);
       const LaneGroup<32> g;
       nk = g.sum(nk);
-      // slot mode (vslot): values at their natural index in the block's slot, packed
-      // afterwards (compact_generic_kernel); else a per-block look-back chain
-      uint64_t prefix = 0;
-      bool fits = true;
-      if (!A.vslot) {
-        prefix = warp_lookback(A.ws.status, tile, nk, A.ws.epoch);
-        fits = A.val_off + 8 * (prefix + nk) <= A.cap;
-      }
+      // values go to the block's slot at their natural index (A.vslot, always set by the
+      // host) and are packed afterwards by compact_generic_kernel, which also checks the
+      // stream capacity
       if (lane == 0) {
         counts[blk] = nk;
         if (blk + 1 == A.nblocks) for (uint64_t pb = A.nblocks; pb < ((A.nblocks + 3) & ~3ull); ++pb) counts[pb] = 0;
-        if (!fits) atomicOr(A.ws.flags, kFlagOverflow);
         A.ws.partials[blk * 4 + 0] = nf ? 0.0 : ldexp((double)T, -2 * k);
         A.ws.partials[blk * 4 + 1] = nf ? 0.0 : ldexp((double)hd, -2 * k);
-        misc[1] = prefix;
-        misc[2] = fits;
       }
       for (int w = lane; w < W; w += 32) masks[blk * W + w] = maskw[w];
     }
     __syncthreads();
-    if (A.vslot) {
-      double* slot = A.vslot + blk * (uint64_t)N3;
-      for (int p = tid; p < N3; p += kGenCThreads)
-        if ((maskw[p >> 6] >> (p & 63)) & 1ull) slot[p] = u[p];
-    } else if (misc[2]) {
-      // kept values in ascending index: rank = popcount of lower mask bits
-      const uint64_t prefix = misc[1];
-      for (int p = tid; p < N3; p += kGenCThreads) {
-        const uint64_t mw = maskw[p >> 6];
-        if ((mw >> (p & 63)) & 1ull) {
-          uint32_t rank = (uint32_t)__popcll(mw & ((1ull << (p & 63)) - 1ull));
-          for (int w = 0; w < (p >> 6); ++w) rank += (uint32_t)__popcll(maskw[w]);
-          vals[prefix + rank] = u[p];
-        }
-      }
-    }
+    double* slot = A.vslot + blk * (uint64_t)N3;
+    for (int p = tid; p < N3; p += kGenCThreads)
+      if ((maskw[p >> 6] >> (p & 63)) & 1ull) slot[p] = u[p];
   }
 }
 

@@ -210,9 +210,6 @@ cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_
 }
 
 template <int LX>
-size_t gen_smem() { return GenSmem<LX>::bytes; }
-
-template <int LX>
 int launch_compress_generic(isf_lossy_plan* p, CompressArgs a, cudaStream_t s) {
   const size_t sm = GenSmem<LX>::bytes;
   static bool attr_set[64] = {};
