@@ -88,11 +88,9 @@ __device__ __forceinline__ uint32_t claim_tile(uint32_t* counter) {
 }
 
 // --------------------------- generic (any lx, comps) ------------------------
-#ifndef ISF_GEN_CTHREADS
-#define ISF_GEN_CTHREADS 32
-#endif
-// compress_generic: one warp per block (selection is one warp's job, so wider CTAs idle)
-constexpr int kGenCThreads = ISF_GEN_CTHREADS;
+// compress_generic: one warp per block (selection is one warp's job, so wider CTAs idle;
+// 64 and 128 threads measured slower on the cfg4 sweep)
+constexpr int kGenCThreads = 32;
 // decompress_generic CTA width per lx (measured on the cfg4 sweep, profiles/r1_summary.md):
 // small blocks want more CTAs, large ones more threads per block
 template <int LX>
@@ -290,15 +288,18 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* counts = reinterpret_cast<uint32_t*>(A.stream);
   uint64_t* masks = reinterpret_cast<uint64_t*>(A.stream + A.mask_off);
+  // block tickets one ahead: the next block's atomic is in flight while this one runs
+  uint32_t next = 0;
+  if (lane == 0) next = atomicAdd(A.ws.counter, 1u);
+  next = __shfl_sync(0xffffffffu, next, 0);
   for (;;) {
-    __syncthreads();
-    if (tid == 0) misc[0] = atomicAdd(A.ws.counter, 1u);
-    __syncthreads();
-    const uint32_t tile = (uint32_t)misc[0];
+    const uint32_t tile = next;
     if (tile >= A.ws.ntiles) {
-      if (tid == 0 && tile == A.ws.ntiles + A.ws.total_warps - 1) *A.ws.counter = 0;
+      if (lane == 0 && tile == A.ws.ntiles + A.ws.total_warps - 1) *A.ws.counter = 0;
       break;
     }
+    if (lane == 0) next = atomicAdd(A.ws.counter, 1u);
+    __syncwarp();  // the previous block's smem is consumed
     const uint64_t blk = tile;
     const uint64_t e = blk / A.comps, c = blk % A.comps;
     const double* src = A.field + e * (uint64_t)N3 * A.comps + c;
@@ -356,6 +357,7 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
     double* slot = A.vslot + blk * (uint64_t)N3;
     for (int p = tid; p < N3; p += kGenCThreads)
       if ((maskw[p >> 6] >> (p & 63)) & 1ull) slot[p] = u[p];
+    next = __shfl_sync(0xffffffffu, next, 0);
   }
 }
 
