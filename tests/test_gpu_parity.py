@@ -36,9 +36,20 @@ def _assert_stream_parity(oracle, blk, ref, P, comps, eps, coeffs=None):
         return 0
     # near-threshold acceptance rule: a differing block is accepted only if the
     # oracle with eps^2*T perturbed by +-4*2^-52*P^3 reproduces the GPU kept count.
-    gc, gm, _ = oracle.parse_stream(got, P, B)
-    rc_, rm, _ = oracle.parse_stream(ref, P, B)
+    gc, gm, gv = oracle.parse_stream(got, P, B)
+    rc_, rm, rv = oracle.parse_stream(ref, P, B)
     bad = np.nonzero((gc != rc_) | np.any(gm != rm, axis=1))[0]
+    # every block with the oracle's count and mask carries bit-identical values
+    go = np.concatenate([[0], np.cumsum(gc.astype(np.int64))])
+    ro = np.concatenate([[0], np.cumsum(rc_.astype(np.int64))])
+    ok_blk = np.ones(B, bool)
+    ok_blk[bad] = False
+    for b in np.nonzero(ok_blk)[0]:
+        if gc[b]:
+            assert np.array_equal(np.asarray(gv[go[b]:go[b + 1]]).view(np.uint64),
+                                  np.asarray(rv[ro[b]:ro[b + 1]]).view(np.uint64)), f"block {b}: values differ"
+    if bad.size == 0:
+        assert got.size == ref.size and np.array_equal(got, ref), "stream bytes differ outside the value records"
     assert coeffs is not None, f"{bad.size} blocks differ"
     rel = 4 * 2.0 ** -52 * P ** 3
     for b in bad:
@@ -270,6 +281,19 @@ def test_c_abi_allreduce_single_rank(native):
             assert torch.equal(st.view(torch.int64)[:11], ref.view(torch.int64)[:11]), status
     finally:
         nccl.ncclCommDestroy(comm)
+
+
+@pytest.mark.parametrize("P", [3, 4, 6, 10, 12])
+def test_generic_decompress_bitexact(native, oracle, P):
+    """The generic (lx != 8) decode + inverse DLT is bit-identical to the oracle's."""
+    nb = 64
+    u = oracle.gen_spectral(P, nb)
+    for eps in (1e-2, 1e-6):
+        f, blk, ref, st = _compress_both(native, oracle, u, P, 1, eps)
+        back = native.lossy_decompress(blk, f.shape)
+        rc, ob, _ = oracle.decompress(blk.stream.cpu().numpy(), P, 1, nb)
+        assert rc == 0
+        assert np.array_equal(back.values.cpu().numpy().view(np.uint64), ob.view(np.uint64)), (P, eps)
 
 
 @pytest.mark.parametrize("case", ["tgv", "spectral_dense", "tiny_values", "signed_zeros"])
