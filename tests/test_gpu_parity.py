@@ -445,3 +445,35 @@ def test_status_flags_all_schedules(native, oracle, P, mode):
     assert int(si[10].item()) == 0
     rc, ref, _ = oracle.compress(u, P, 1, 1e-3)
     assert np.array_equal(st[: int(si[8].item())].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("P", [6, 12])
+def test_generic_large_sampled_parity(native, oracle, P):
+    """cfg4-sized generic path (32,768 elements): deterministic streams, the L2 bound,
+    plain decode == decode with error report, and the first / last 128 blocks of the
+    stream (counts, masks, value records) bit-identical to the oracle's stream of the
+    same blocks (offsets at full size)."""
+    import paper_2407_20731_b200 as PK
+    n, S = 32768, 128
+    plan = PK.get_plan(P, 1, 0)
+    vals = torch.empty(n * P ** 3, dtype=torch.float64, device="cuda")
+    plan.generate_spectral(vals, n, 0, oracle.SPECTRAL_SEED, oracle.spectral_amplitudes(P))
+    f = PK.Field(32, P, 1, vals)
+    eps = 1e-3
+    a = PK.lossy_compress(f, PK.LossyConfig(eps))
+    b = PK.lossy_compress(f, PK.LossyConfig(eps))
+    assert torch.equal(a.stream, b.stream)
+    back, rep = PK.decompress_with_error(a, f.shape, f)
+    plain = PK.lossy_decompress(a, f.shape)
+    assert torch.equal(back.values.view(torch.int64), plain.values.view(torch.int64))
+    assert 0 < rep.rel_l2 <= eps * (1 + 1e-9)
+    got = a.stream.cpu().numpy()
+    gc, gm, gv = oracle.parse_stream(got, P, n)
+    go = np.concatenate([[0], np.cumsum(gc.astype(np.int64))])
+    for b0 in (0, n - S):
+        u = oracle.gen_spectral(P, S, block0=b0)
+        rc, ref, _ = oracle.compress(u, P, 1, eps)
+        assert rc == 0
+        rc_, rm, rv = oracle.parse_stream(ref, P, S)
+        assert np.array_equal(gc[b0:b0 + S], rc_) and np.array_equal(gm[b0:b0 + S], rm)
+        assert np.array_equal(np.asarray(gv[go[b0]:go[b0 + S]]).view(np.uint64), np.asarray(rv).view(np.uint64))
