@@ -524,20 +524,48 @@ struct FinalizeArgs {
 };
 
 constexpr int kFinThreads = 512;
+constexpr int kFinChunks = 256;  // first-level CTAs of finalize_pre_kernel
 
-__global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinalizeArgs A) {
-  __shared__ double s0[kFinThreads], s1[kFinThreads];
-  __shared__ unsigned long long m0[kFinThreads], m1[kFinThreads];
+// CTA-wide fixed-order reduction of records [begin, end) (sums of .0/.1, max of the bit
+// patterns of .2/.3 when mode == 1); the results are in s0[0], s1[0], m0[0], m1[0]
+__device__ __forceinline__ void reduce_records(const double* partials, uint64_t begin, uint64_t end, int mode,
+                                               double* s0, double* s1, unsigned long long* m0,
+                                               unsigned long long* m1) {
   const int t = threadIdx.x;
   double a0 = 0.0, a1 = 0.0;
   unsigned long long x0 = 0, x1 = 0;
-  for (uint64_t i = t; i < A.nparts; i += kFinThreads) {
-    a0 = __dadd_rn(a0, A.partials[i * 4 + 0]);
-    a1 = __dadd_rn(a1, A.partials[i * 4 + 1]);
-    if (A.mode == 1) {
-      unsigned long long v = (unsigned long long)__double_as_longlong(A.partials[i * 4 + 2]);
+  // 8 records in flight per thread, summed in the same sequential order as the tail loop
+  // (the statistics stay bit-identical to a plain strided loop; the generic compress
+  // path reduces one record per block here)
+  const double2* rec = reinterpret_cast<const double2*>(partials);
+  uint64_t i0 = begin + t;
+  constexpr int U = 8;
+  for (; i0 + (uint64_t)(U - 1) * kFinThreads < end; i0 += (uint64_t)U * kFinThreads) {
+    double2 lo[U], hi[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      lo[j] = rec[(i0 + (uint64_t)j * kFinThreads) * 2];
+      if (mode == 1) hi[j] = rec[(i0 + (uint64_t)j * kFinThreads) * 2 + 1];
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      a0 = __dadd_rn(a0, lo[j].x);
+      a1 = __dadd_rn(a1, lo[j].y);
+      if (mode == 1) {
+        unsigned long long v = (unsigned long long)__double_as_longlong(hi[j].x);
+        x0 = v > x0 ? v : x0;
+        v = (unsigned long long)__double_as_longlong(hi[j].y);
+        x1 = v > x1 ? v : x1;
+      }
+    }
+  }
+  for (uint64_t i = i0; i < end; i += kFinThreads) {
+    a0 = __dadd_rn(a0, partials[i * 4 + 0]);
+    a1 = __dadd_rn(a1, partials[i * 4 + 1]);
+    if (mode == 1) {
+      unsigned long long v = (unsigned long long)__double_as_longlong(partials[i * 4 + 2]);
       x0 = v > x0 ? v : x0;
-      v = (unsigned long long)__double_as_longlong(A.partials[i * 4 + 3]);
+      v = (unsigned long long)__double_as_longlong(partials[i * 4 + 3]);
       x1 = v > x1 ? v : x1;
     }
   }
@@ -552,6 +580,31 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinalizeArgs A) {
     }
     __syncthreads();
   }
+}
+
+// First level of the statistics reduction when there is one record per block (generic
+// compress): CTA c reduces the fixed record range [c * CH, (c + 1) * CH) into record c of
+// `out`, which finalize_kernel then reduces (a deterministic two-level tree)
+__global__ void __launch_bounds__(kFinThreads) finalize_pre_kernel(const double* partials, uint64_t nparts, int mode,
+                                                                  double* out) {
+  __shared__ double s0[kFinThreads], s1[kFinThreads];
+  __shared__ unsigned long long m0[kFinThreads], m1[kFinThreads];
+  const uint64_t ch = (nparts + gridDim.x - 1) / gridDim.x;
+  const uint64_t lo = (uint64_t)blockIdx.x * ch, hi = lo + ch < nparts ? lo + ch : nparts;
+  reduce_records(partials, lo < nparts ? lo : nparts, hi, mode, s0, s1, m0, m1);
+  if (threadIdx.x == 0) {
+    out[blockIdx.x * 4 + 0] = s0[0];
+    out[blockIdx.x * 4 + 1] = s1[0];
+    out[blockIdx.x * 4 + 2] = __longlong_as_double((long long)m0[0]);
+    out[blockIdx.x * 4 + 3] = __longlong_as_double((long long)m1[0]);
+  }
+}
+
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(FinalizeArgs A) {
+  __shared__ double s0[kFinThreads], s1[kFinThreads];
+  __shared__ unsigned long long m0[kFinThreads], m1[kFinThreads];
+  const int t = threadIdx.x;
+  reduce_records(A.partials, 0, A.nparts, A.mode, s0, s1, m0, m1);
   if (t == 0) {
     double* st = reinterpret_cast<double*>(A.stats);
     uint64_t* su = reinterpret_cast<uint64_t*>(A.stats);

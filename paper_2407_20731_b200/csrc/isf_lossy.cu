@@ -174,7 +174,8 @@ int ensure(isf_lossy_plan* p, size_t ntiles, size_t nparts, size_t noff) {
   if (nparts > p->partials_cap) {
     if (p->partials) cudaFree(p->partials);
     size_t cap = std::max<size_t>(nparts, 1024);
-    CUDA_TRY(cudaMalloc(&p->partials, cap * 4 * sizeof(double)));
+    // + kFinChunks records of scratch for the two-level statistics reduction
+    CUDA_TRY(cudaMalloc(&p->partials, (cap + kFinChunks) * 4 * sizeof(double)));
     p->partials_cap = cap;
   }
   return 0;
@@ -516,6 +517,14 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   }
   FinalizeArgs f{0, p->partials, parts, p->status, total_ptr, ntiles, p->flags, d_stats, B,
                  B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
+  if (parts >= 16 * (uint64_t)kFinChunks) {  // one record per block: reduce on many SMs first
+    double* scratch = p->partials + p->partials_cap * 4;
+    finalize_pre_kernel<<<kFinChunks, kFinThreads, 0, s>>>(p->partials, parts, 0, scratch);
+    CUDA_TRY(cudaGetLastError());
+    f.partials = scratch;
+    f.nparts = kFinChunks;
+    ++launches;
+  }
   finalize_kernel<<<1, kFinThreads, 0, s>>>(f);
   CUDA_TRY(cudaGetLastError());
   p->last_launches = launches;
