@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(gen_dthreads<LX>()) decompress_generic(Decompr
     const double* org = A.orig ? A.orig + e * (uint64_t)N3 * A.comps + c : nullptr;
     for (int p = tid; p < N3; p += kT) {
       const double val = __dadd_rn(u[p], 0.0);  // zero results are written as +0
-      dst[(uint64_t)p * A.comps] = val;
+      __stcs(dst + (uint64_t)p * A.comps, val);  // streaming: the field is not re-read here
       if (org) {
         const int x = p % N, yy = (p / N) % N, z = p / N2;
         const double w3 = __dmul_rn(__dmul_rn(Wg<LX>(x), Wg<LX>(yy)), Wg<LX>(z));
