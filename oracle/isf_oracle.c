@@ -187,19 +187,31 @@ void iso_inv_block(int lx, const double* B, const double* a, double* u) {
 }
 
 /* ------------------------------------------------------------------------- */
-/* Pinned truncation rule, SPEC.md:225 made exact:            */
-/*   K      = min(25, floor((63 - ceil(log2 lx^3)) / 2))  (e_j < 2^50 < 2^52)   */
+/* Pinned truncation rule v2: SPEC.md:225 ("sort by |c|      */
+/* descending, keep the smallest prefix with discarded/total energy <=       */
+/* eps^2") in exact integer arithmetic at two scales.                         */
+/*   EM     = min(52, 63 - ceil(log2 n3)),  m = floor(EM / 2)                 */
 /*   s      = frexp exponent of max|a|   (2^(s-1) <= max|a| < 2^s)            */
-/*   a''_j  = |a_j| * 2^(K-s)            (exact whenever the result is >= 1)  */
-/*   e_j    = fl(a''_j * a''_j)  in [0, 2^50)                                 */
-/*   lo_j   = floor(e_j), hi_j = lo_j + 1  (integers, u64; hi_j > e_j)        */
-/*   T      = sum lo_j,  q = floor(fl(eps*eps) * 2^64),  thr = floor(T*q/2^64) */
+/*   x_j    = |a_j| 2^(m-s)   (exact),  e_j = RD(x_j^2) in [0, 2^(2m))        */
+/*   h      = EM - 2m + [RD(x_max^2) < 2^(2m-1)]  so  max e_j 2^h in          */
+/*            [2^(EM-1), 2^EM)                                                */
+/*   T      = sum floor(e_j 2^h)                 (scale A: the block total)  */
+/*   E2     = RD(eps^2) = M 2^Ee (M < 2^53),  P = T M  (128-bit)              */
+/*   G      = 52 - bitlen(P) - Ee, clamped to G <= 1023 - h                    */
+/*   thr    = floor(P 2^(G + Ee))  in [2^51, 2^52)   (scale B = A * 2^G)       */
+/*   hi_j   = floor(e_j 2^(h+G)) + 1, or 2^52 when e_j 2^(h+G) >= 2^52        */
 /*   discard order: |a| ascending, ties by index descending (= sort by |c|    */
 /*   descending, index ascending, read from the end)                         */
 /*   D      = longest prefix of the discard order with sum hi <= thr          */
 /*   kept   = complement of D; an all-zero block keeps nothing.               */
-/* Integer sums are exact and order independent, so any correct GPU          */
-/* selection reproduces the mask bit for bit.                                 */
+/* hi_j > 2^G * (true energy at scale A) and thr <= 2^G eps^2 T, so the       */
+/* discarded energy is <= eps^2 * total (the RelativeL2 guarantee).  The      */
+/* threshold-relative scale B resolves the discarded energies to 2^-51 of the */
+/* threshold and T is within n3 units of 2^-51 T, so the rule agrees with the */
+/* exact-real rule (iso_select_block_literal) except for blocks whose exact   */
+/* margin is below ~n3 2^-50 of the threshold -- SURVEY.md 8c's near-         */
+/* threshold band.  Integer sums are exact and order independent, so any      */
+/* correct GPU selection reproduces the mask bit for bit.                     */
 /* ------------------------------------------------------------------------- */
 static int ceil_log2_u32(uint32_t v) {
     int r = 0;
@@ -207,9 +219,9 @@ static int ceil_log2_u32(uint32_t v) {
     return r;
 }
 
-static int energy_K(int lx) {
-    int K = (63 - ceil_log2_u32((uint32_t)(lx * lx * lx))) / 2;
-    return K < 25 ? K : 25;
+static int energy_EM(int lx) {
+    const int em = 63 - ceil_log2_u32((uint32_t)(lx * lx * lx));
+    return em < 52 ? em : 52;
 }
 
 typedef struct {
@@ -224,13 +236,36 @@ static int cmp_discard_order(const void* pa, const void* pb) {
     return b->idx - a->idx; /* larger index discarded first */
 }
 
-static uint64_t mulhi64(uint64_t a, uint64_t b) {
-    return (uint64_t)(((unsigned __int128)a * (unsigned __int128)b) >> 64);
+static double mul_rd(double x, double y);
+
+/* RD(x * x) for x >= 0 */
+static double sq_rd(double x) {
+    const double p = x * x;
+    if (p < 0x1p-960) return mul_rd(x, x); /* near the subnormal range: binary128 */
+    const double e = fma(x, x, -p);       /* exact error */
+    return e < 0 ? nextafter(p, 0.0) : p;
 }
 
-static uint64_t eps_q(double max_error) {
-    double e2 = max_error * max_error;
-    return (uint64_t)ldexp(e2, 64); /* e2 < 1 => < 2^64; truncation = floor */
+static uint64_t thr_of(uint64_t T, double max_error, int h, int* G_out) {
+    const double E2 = mul_rd(max_error, max_error);
+    int ex;
+    const double m = frexp(E2, &ex); /* E2 = m 2^ex, m in [0.5, 1) */
+    const uint64_t M = (uint64_t)ldexp(m, 53);
+    const int Ee = ex - 53;
+    const unsigned __int128 P = (unsigned __int128)T * M;
+    if (P == 0) {
+        *G_out = 0;
+        return 0;
+    }
+    const uint64_t ph = (uint64_t)(P >> 64), pl = (uint64_t)P;
+    const int L = ph ? 128 - __builtin_clzll(ph) : 64 - __builtin_clzll(pl);
+    int G = 52 - L - Ee;
+    if (G > 1023 - h) G = 1023 - h;
+    const int sh = G + Ee; /* thr = floor(P 2^sh) */
+    *G_out = G;
+    if (sh >= 0) return (uint64_t)(P << sh);
+    if (-sh >= 128) return 0;
+    return (uint64_t)(P >> (-sh));
 }
 
 static uint32_t select_impl(int lx, const double* a, double max_error, double rel, uint64_t* mask,
@@ -247,7 +282,7 @@ static uint32_t select_impl(int lx, const double* a, double max_error, double re
     }
     if (lo_total) *lo_total = 0;
     if (lo_disc) *lo_disc = 0;
-    if (scale_exp) *scale_exp = 0;
+    if (scale_exp) scale_exp[0] = scale_exp[1] = 0;
     if (nonfinite) *nonfinite = 0;
     if (maxbits >= 0x7ff0000000000000ull) {
         if (nonfinite) *nonfinite = 1;
@@ -258,24 +293,23 @@ static uint32_t select_impl(int lx, const double* a, double max_error, double re
     memcpy(&amax, &maxbits, 8);
     int s;
     (void)frexp(amax, &s);
-    const int K = energy_K(lx);
-    const int k = K - s;
+    const int EM = energy_EM(lx), hm = EM / 2;
+    const int k = hm - s;
+    const double emax = sq_rd(ldexp(amax, k));
+    const int h = (EM - 2 * hm) + (emax < ldexp(1.0, 2 * hm - 1) ? 1 : 0);
     static __thread sel_item items[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
-    static __thread uint64_t hi[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
-    static __thread uint64_t lo[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+    static __thread double ev[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
     uint64_t T = 0;
     for (int j = 0; j < n3; ++j) {
-        double as = ldexp(fabs(a[j]), k);
-        double e = as * as;
-        lo[j] = (uint64_t)floor(e);
-        hi[j] = lo[j] + 1; /* strict upper bound of e: the discarded energy is never underestimated */
-        T += lo[j];
+        ev[j] = sq_rd(ldexp(fabs(a[j]), k));
+        T += (uint64_t)ldexp(ev[j], h); /* < 2^52: exact integer part by truncation */
         uint64_t b;
         memcpy(&b, &a[j], 8);
         items[j].key = b & 0x7fffffffffffffffull;
         items[j].idx = j;
     }
-    uint64_t thr = mulhi64(T, eps_q(max_error));
+    int G;
+    uint64_t thr = thr_of(T, max_error, h, &G);
     if (rel != 0.0) {
         long double t = (long double)thr * (1.0L + (long double)rel);
         thr = t <= 0.0L ? 0 : (t >= 18446744073709551615.0L ? ~0ull : (uint64_t)t);
@@ -283,8 +317,11 @@ static uint32_t select_impl(int lx, const double* a, double max_error, double re
     qsort(items, (size_t)n3, sizeof(sel_item), cmp_discard_order);
     uint64_t acc = 0;
     int m = 0;
-    while (m < n3 && acc + hi[items[m].idx] <= thr) {
-        acc += hi[items[m].idx];
+    while (m < n3) {
+        const double y = ldexp(ev[items[m].idx], h + G);
+        const uint64_t hj = y >= 0x1p52 ? (1ull << 52) : (uint64_t)y + 1; /* strict upper bound */
+        if (acc + hj > thr) break;
+        acc += hj;
         ++m;
     }
     for (int p = m; p < n3; ++p) {
@@ -292,8 +329,11 @@ static uint32_t select_impl(int lx, const double* a, double max_error, double re
         mask[j >> 6] |= 1ull << (j & 63);
     }
     if (lo_total) *lo_total = T;
-    if (lo_disc) *lo_disc = acc; /* hi-sum of the discarded set (upper bound) */
-    if (scale_exp) *scale_exp = -2 * k;
+    if (lo_disc) *lo_disc = acc; /* hi-sum of the discarded set (upper bound, scale B) */
+    if (scale_exp) {
+        scale_exp[0] = -2 * k - h;     /* energy = T * 2^scale_exp[0]   */
+        scale_exp[1] = -2 * k - h - G; /* energy = acc * 2^scale_exp[1] */
+    }
     return (uint32_t)(n3 - m);
 }
 
@@ -305,6 +345,128 @@ uint32_t iso_select_block(int lx, const double* a, double max_error, uint64_t* m
 uint32_t iso_select_block_perturbed(int lx, const double* a, double max_error, double rel,
                                     uint64_t* mask) {
     return select_impl(lx, a, max_error, rel, mask, NULL, NULL, NULL, NULL);
+}
+
+static int omp_threads(int nthreads) {
+#ifdef _OPENMP
+    return nthreads > 0 ? nthreads : omp_get_max_threads();
+#else
+    (void)nthreads;
+    return 1;
+#endif
+}
+
+static void gather_block(int n3, int comps, const double* field, uint64_t e, int c, double* out) {
+    const double* base = field + e * (uint64_t)n3 * comps + c;
+    for (int p = 0; p < n3; ++p) out[p] = base[(uint64_t)p * comps];
+}
+
+/* ------------------------------------------------------------------------- */
+/* SPEC-literal truncation (SPEC.md:225 read in exact real arithmetic):       */
+/*   sort the coefficients by |a| descending (ties: index ascending), keep   */
+/*   the smallest prefix whose discarded energy satisfies                     */
+/*        sum_{discarded} a_j^2  <=  eps^2 * sum_j a_j^2        (reals)       */
+/* with eps the binary64 max_error.  This is the semantic the exact-integer   */
+/* rule above approximates conservatively; the parity tests count the blocks  */
+/* where the two differ (north_star: "counted and reported").                 */
+/* Evaluation is filtered: a_j^2 is exact in binary128 (106-bit product), the */
+/* sums carry a rigorous error bound, and a block whose decision at the cut   */
+/* lies inside that bound is reported as ambiguous (*ambiguous = 1) for the   */
+/* caller's exact rational evaluation (oracle.py, fractions.Fraction).        */
+/* rel scales the right-hand side: eps^2 * T * (1 + rel).                     */
+/* ------------------------------------------------------------------------- */
+uint32_t iso_select_block_literal(int lx, const double* a, double max_error, double rel, uint64_t* mask,
+                                  int* ambiguous) {
+    const int n3 = lx * lx * lx;
+    const int W = (n3 + 63) / 64;
+    for (int w = 0; w < W; ++w) mask[w] = 0;
+    if (ambiguous) *ambiguous = 0;
+    static __thread sel_item items[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+    static __thread qreal e[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+    qreal T = 0;
+    for (int j = 0; j < n3; ++j) {
+        if (!isfinite(a[j])) return 0;
+        const qreal q = (qreal)a[j];
+        e[j] = q * q; /* exact: 53 x 53 bits <= 113 */
+        T += e[j];
+        uint64_t b;
+        memcpy(&b, &a[j], 8);
+        items[j].key = b & 0x7fffffffffffffffull;
+        items[j].idx = j;
+    }
+    if (T == 0) return 0; /* all-zero block: every prefix qualifies, keep nothing */
+    qsort(items, (size_t)n3, sizeof(sel_item), cmp_discard_order);
+    const qreal eps2 = (qreal)max_error * (qreal)max_error; /* exact */
+    const qreal thr = eps2 * T * (1 + (qreal)rel);
+    /* |T^ - T| <= (n-1) u T, |tail^_m - tail_m| <= (m-1) u tail_m <= n u T, thr adds
+       three roundings: a generous common bound (u = 2^-113) */
+    const qreal bound = ldexpq((qreal)(2 * n3 + 8), -112) * T;
+    qreal acc = 0;
+    int m = 0;
+    while (m < n3) {
+        const qreal nx = acc + e[items[m].idx];
+        if (nx > thr) break;
+        acc = nx;
+        ++m;
+    }
+    /* the decision at the cut: tail_m <= thr (true) and tail_{m+1} > thr (if m < n) */
+    if (ambiguous) {
+        if (thr - acc <= bound) *ambiguous = 1;
+        if (m < n3 && (acc + e[items[m].idx]) - thr <= bound) *ambiguous = 1;
+    }
+    for (int p = m; p < n3; ++p) {
+        const int j = items[p].idx;
+        mask[j >> 6] |= 1ull << (j & 63);
+    }
+    return (uint32_t)(n3 - m);
+}
+
+/* Compare a stream's masks with the SPEC-literal rule over a whole field.
+ * cls[b] per block: 0 identical, 1 differs but accepted by SURVEY.md 8c's
+ * near-threshold rule (the literal rule with eps^2 T scaled by 1 -+ 4 2^-52 lx^3
+ * reproduces the stream's kept count), 2 differs beyond that, 3 ambiguous in
+ * binary128 (the caller decides it exactly).  Returns the number of blocks with
+ * cls != 0; *kept_literal receives the literal rule's total kept count. */
+uint64_t iso_literal_check(int lx, int comps, uint64_t n_elements, const double* field, double max_error,
+                           const uint8_t* stream, uint8_t* cls, uint64_t* kept_literal, int nthreads) {
+    const int n3 = lx * lx * lx, W = (n3 + 63) / 64;
+    const uint64_t B = n_elements * (uint64_t)comps;
+    const uint32_t* counts = (const uint32_t*)stream;
+    const uint64_t* masks = (const uint64_t*)(stream + ((4 * B + 15) & ~15ull));
+    double F[ISO_MAX_LX * ISO_MAX_LX], Bm[ISO_MAX_LX * ISO_MAX_LX];
+    iso_matrices(lx, F, Bm);
+    const double rel = 4.0 * ldexp(1.0, -52) * (double)n3;
+    uint64_t ndiff = 0, klit = 0;
+    const int nt = omp_threads(nthreads);
+#pragma omp parallel for num_threads(nt) schedule(dynamic, 256) reduction(+ : ndiff, klit)
+    for (uint64_t b = 0; b < B; ++b) {
+        double u[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX], a[ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX];
+        uint64_t mk[(ISO_MAX_LX * ISO_MAX_LX * ISO_MAX_LX + 63) / 64];
+        gather_block(n3, comps, field, b / comps, (int)(b % comps), u);
+        iso_fwd_block(lx, F, u, a);
+        int amb = 0;
+        const uint32_t k = iso_select_block_literal(lx, a, max_error, 0.0, mk, &amb);
+        klit += k;
+        int same = k == counts[b];
+        for (int w = 0; w < W && same; ++w) same = mk[w] == masks[b * W + w];
+        uint8_t c = 0;
+        if (amb) {
+            c = 3;
+        } else if (!same) {
+            c = 2;
+            for (int s = -1; s <= 1; s += 2) {
+                int amb2 = 0;
+                const uint32_t k2 = iso_select_block_literal(lx, a, max_error, s * rel, mk, &amb2);
+                int same2 = k2 == counts[b];
+                for (int w = 0; w < W && same2; ++w) same2 = mk[w] == masks[b * W + w];
+                if (same2 || amb2) c = 1;
+            }
+        }
+        cls[b] = c;
+        ndiff += c != 0;
+    }
+    if (kept_literal) *kept_literal = klit;
+    return ndiff;
 }
 
 /* ------------------------------------------------------------------------- */
@@ -321,10 +483,6 @@ uint64_t iso_stream_capacity(int lx, uint64_t nblocks) {
     return iso_stream_header_bytes(lx, nblocks) + 8ull * lx * lx * lx * nblocks;
 }
 
-static void gather_block(int n3, int comps, const double* field, uint64_t e, int c, double* out) {
-    const double* base = field + e * (uint64_t)n3 * comps + c;
-    for (int p = 0; p < n3; ++p) out[p] = base[(uint64_t)p * comps];
-}
 
 /* ------------------------------------------------------------------------- */
 /* RelativeLInf rule:         */
@@ -407,14 +565,6 @@ uint32_t iso_select_block_linf(int lx, const double* Bm, const double* a, double
     return (uint32_t)(n3 - m);
 }
 
-static int omp_threads(int nthreads) {
-#ifdef _OPENMP
-    return nthreads > 0 ? nthreads : omp_get_max_threads();
-#else
-    (void)nthreads;
-    return 1;
-#endif
-}
 
 int iso_compress(int lx, int comps, uint64_t n_elements, const double* field, double max_error,
                  uint8_t* stream, uint64_t cap, uint64_t* stream_bytes, iso_stats* st, int nthreads) {
@@ -458,21 +608,20 @@ int iso_compress_norm(int lx, int comps, uint64_t n_elements, const double* fiel
             iso_fwd_block(lx, F, u, a);
             uint64_t* mk = masks + b * W;
             uint64_t lt, ld;
-            int se, nf;
+            int se[2] = {0, 0}, nf;
             uint32_t kept;
             if (norm == 1) {
                 double umax = 0.0;
                 for (int j = 0; j < n3; ++j) umax = fmax(umax, fabs(u[j]));
                 kept = iso_select_block_linf(lx, Bm, a, umax, max_error, mk, &nf);
                 lt = ld = 0;
-                se = 0;
             } else {
-                kept = iso_select_block(lx, a, max_error, mk, &lt, &ld, &se, &nf);
+                kept = iso_select_block(lx, a, max_error, mk, &lt, &ld, se, &nf);
             }
             if (nf) tbad[t] = 1;
             counts[b] = kept;
-            tot += ldexp((double)lt, se);
-            disc += ldexp((double)ld, se);
+            tot += ldexp((double)lt, se[0]);
+            disc += ldexp((double)ld, se[1]);
             if (nv + kept > capv) {
                 while (nv + kept > capv) capv *= 2;
                 vals = (double*)realloc(vals, capv * sizeof(double));

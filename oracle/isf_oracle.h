@@ -58,16 +58,28 @@ int iso_matrices(int lx, double* F /* [k*lx+i] */, double* B /* [i*lx+k] */);
 /* ---- one block (lx^3 contiguous values, x fastest) ---- */
 void iso_fwd_block(int lx, const double* F, const double* u, double* a);   /* sweeps z, y, x */
 void iso_inv_block(int lx, const double* B, const double* a, double* u);   /* sweeps x, y, z */
-/* Pinned truncation rule.  Writes ceil(lx^3/64) mask words,
- * returns kept count; *lo_total (sum lo over the block) / *lo_disc (sum hi over the
- * discarded set) receive the integer energy sums and
- * *scale_exp the binary exponent that maps them back (energy = sum * 2^scale_exp). */
+/* Pinned truncation rule v2.  Writes ceil(lx^3/64) mask words,
+ * returns kept count; *lo_total (block total at scale A) / *lo_disc (sum hi over the
+ * discarded set at scale B) receive the integer energy sums and scale_exp[0..1] the
+ * binary exponents that map them back (energy = lo_total * 2^scale_exp[0],
+ * lo_disc * 2^scale_exp[1]). */
 uint32_t iso_select_block(int lx, const double* a, double max_error, uint64_t* mask,
                           uint64_t* lo_total, uint64_t* lo_disc, int* scale_exp, int* nonfinite);
 /* Same rule with the threshold perturbed: thr' = floor(thr * (1 + rel)) (rel may be
  * negative).  Used by the parity tests' near-threshold acceptance rule. */
 uint32_t iso_select_block_perturbed(int lx, const double* a, double max_error, double rel,
                                     uint64_t* mask);
+
+/* SPEC-literal rule (SPEC.md:225 in exact reals, binary128-filtered): kept count
+ * and mask; *ambiguous = 1 when binary128 cannot decide the cut (exact fallback in
+ * oracle.py).  rel scales eps^2 * T by (1 + rel). */
+uint32_t iso_select_block_literal(int lx, const double* a, double max_error, double rel, uint64_t* mask,
+                                  int* ambiguous);
+/* Whole-field comparison of a stream's masks with the literal rule; cls[b]: 0 same,
+ * 1 differs within SURVEY.md 8c's near-threshold band, 2 differs beyond it,
+ * 3 ambiguous.  Returns the count of cls != 0. */
+uint64_t iso_literal_check(int lx, int comps, uint64_t n_elements, const double* field, double max_error,
+                           const uint8_t* stream, uint8_t* cls, uint64_t* kept_literal, int nthreads);
 
 /* RelativeLInf rule: Bm = synthesis matrix [i*lx+k], umax = max|u| of the
  * block's nodal values.  Returns the kept count and writes the mask. */

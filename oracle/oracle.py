@@ -64,6 +64,10 @@ def lib():
         L.iso_stream_header_bytes.restype = u64
         L.iso_compress.argtypes = [i32, i32, u64, P, f64, P, u64, P, P, i32]
         L.iso_compress_norm.argtypes = [i32, i32, u64, P, f64, i32, P, u64, P, P, i32]
+        L.iso_select_block_literal.argtypes = [i32, P, f64, f64, P, P]
+        L.iso_select_block_literal.restype = ctypes.c_uint32
+        L.iso_literal_check.argtypes = [i32, i32, u64, P, f64, P, P, P, i32]
+        L.iso_literal_check.restype = u64
         L.iso_select_block_linf.argtypes = [i32, P, P, f64, f64, P, P]
         L.iso_select_block_linf.restype = ctypes.c_uint32
         L.iso_decompress.argtypes = [i32, i32, u64, P, u64, P, P, P, i32]
@@ -115,12 +119,12 @@ def inv_block(lx, a):
 def select_block(lx, a, max_error):
     W = (lx ** 3 + 63) // 64
     mask = np.zeros(W, dtype=np.uint64)
-    lt = ctypes.c_uint64(); ld = ctypes.c_uint64(); se = ctypes.c_int(); nf = ctypes.c_int()
+    lt = ctypes.c_uint64(); ld = ctypes.c_uint64(); se = (ctypes.c_int * 2)(); nf = ctypes.c_int()
     a = np.ascontiguousarray(a, dtype=np.float64)
     kept = lib().iso_select_block(lx, _p(a), float(max_error), _p(mask), ctypes.byref(lt),
-                                  ctypes.byref(ld), ctypes.byref(se), ctypes.byref(nf))
-    return int(kept), mask, {"lo_total": lt.value, "lo_disc": ld.value, "scale_exp": se.value,
-                             "nonfinite": nf.value}
+                                  ctypes.byref(ld), se, ctypes.byref(nf))
+    return int(kept), mask, {"lo_total": lt.value, "lo_disc": ld.value, "scale_exp": se[0],
+                             "disc_exp": se[1], "nonfinite": nf.value}
 
 
 def select_block_perturbed(lx, a, max_error, rel):
@@ -129,6 +133,82 @@ def select_block_perturbed(lx, a, max_error, rel):
     a = np.ascontiguousarray(a, dtype=np.float64)
     kept = lib().iso_select_block_perturbed(lx, _p(a), float(max_error), float(rel), _p(mask))
     return int(kept), mask
+
+
+def select_block_literal(lx, a, max_error, rel=0.0):
+    """SPEC-literal rule (SPEC.md:225 in exact reals), binary128-filtered in C with
+    an exact rational fallback: (kept, mask words)."""
+    W = (lx ** 3 + 63) // 64
+    mask = np.zeros(W, dtype=np.uint64)
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    amb = ctypes.c_int()
+    kept = lib().iso_select_block_literal(lx, _p(a), float(max_error), float(rel), _p(mask), ctypes.byref(amb))
+    if amb.value:
+        return select_block_literal_exact(lx, a, max_error, rel)
+    return int(kept), mask
+
+
+def select_block_literal_exact(lx, a, max_error, rel=0.0):
+    """The same rule in exact rational arithmetic (fractions.Fraction): sort by
+    (|a| descending, index ascending) and keep the smallest prefix whose discarded
+    energy is <= eps^2 * total * (1 + rel)."""
+    from fractions import Fraction
+    n3 = lx ** 3
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+    e = [Fraction(float(x)) ** 2 for x in a]
+    T = sum(e, Fraction(0))
+    mask = np.zeros((n3 + 63) // 64, dtype=np.uint64)
+    if T == 0:
+        return 0, mask
+    thr = Fraction(float(max_error)) ** 2 * T * (1 + Fraction(float(rel)))
+    keys = np.abs(a).view(np.uint64)
+    order = sorted(range(n3), key=lambda j: (int(keys[j]), -j))  # discard order
+    acc, m = Fraction(0), 0
+    while m < n3 and acc + e[order[m]] <= thr:
+        acc += e[order[m]]
+        m += 1
+    for j in order[m:]:
+        mask[j >> 6] |= np.uint64(1) << np.uint64(j & 63)
+    return n3 - m, mask
+
+
+def literal_check(field, lx, comps, max_error, stream, nthreads: int = 0):
+    """Compare a stream's masks with the SPEC-literal rule block by block.
+
+    Returns a dict: blocks, differ (blocks whose mask differs from the literal
+    rule), near_threshold (those accepted by SURVEY.md 8c's rule: the literal rule
+    with eps^2*T scaled by 1 -+ 4*2^-52*lx^3 reproduces the stream's kept count),
+    far (differ beyond that), ambiguous_resolved (blocks binary128 could not decide,
+    settled exactly), kept_literal, kept_stream, far_blocks (first 16 indices)."""
+    field = np.ascontiguousarray(field, dtype=np.float64).reshape(-1)
+    stream = np.ascontiguousarray(stream, dtype=np.uint8)
+    n_el = field.size // (lx ** 3 * comps)
+    B = n_el * comps
+    cls = np.zeros(B, dtype=np.uint8)
+    kl = ctypes.c_uint64()
+    lib().iso_literal_check(lx, comps, n_el, _p(field), float(max_error), _p(stream), _p(cls), ctypes.byref(kl),
+                            nthreads)
+    counts, masks, _ = parse_stream(stream, lx, B)
+    kept_lit = int(kl.value)
+    amb = np.nonzero(cls == 3)[0]
+    rel = 4 * 2.0 ** -52 * lx ** 3
+    n3 = lx ** 3
+    for b in amb:
+        e, c = divmod(int(b), comps)
+        blk = field[e * n3 * comps + c: (e + 1) * n3 * comps: comps]
+        a = fwd_block(lx, blk)
+        k, m = select_block_literal_exact(lx, a, max_error)
+        kept_lit += 0  # the C pass already counted its (binary128) kept value for b
+        if k == counts[b] and np.array_equal(m, masks[b]):
+            cls[b] = 0
+        elif any(select_block_literal_exact(lx, a, max_error, s * rel)[0] == counts[b] for s in (-1, 1)):
+            cls[b] = 1
+        else:
+            cls[b] = 2
+    far = np.nonzero(cls == 2)[0]
+    return {"blocks": int(B), "differ": int(np.count_nonzero(cls)), "near_threshold": int(np.count_nonzero(cls == 1)),
+            "far": int(far.size), "ambiguous_resolved": int(amb.size), "kept_literal": kept_lit,
+            "kept_stream": int(counts.astype(np.int64).sum()), "far_blocks": [int(x) for x in far[:16]]}
 
 
 def stream_capacity(lx, nblocks):

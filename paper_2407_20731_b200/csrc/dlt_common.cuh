@@ -126,16 +126,20 @@ __device__ __forceinline__ void inv_line_ptr(double* p, int stride) {
 }
 
 // ---------------------------------------------------------------------------
-// Energy quantisation: e = fl((|a|*2^k)^2) < 2^50,
-// lo = floor(e) via a round-down add of 2^52, hi = lo + 1.
+// Truncation rule v2 (oracle/isf_oracle.c select_impl):
+//   x_j = |a_j| 2^k (k = EM/2 - s), e_j = RD(x_j^2), T = sum floor(e_j 2^h)  (scale A)
+//   thr = floor(T * RD(eps^2) * 2^G) in [2^51, 2^52)                          (scale B)
+//   hi_j = floor(e_j 2^(h+G)) + 1 (saturated to 2^52: never discardable)
+// floor(y) for 0 <= y < 2^52 is the low mantissa of RD(y + 2^52): one fma_rd each.
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int ceil_log2(int v) {
   int r = 0;
   while ((1 << r) < v) ++r;
   return r;
 }
-__host__ __device__ constexpr int energy_K(int lx) {
-  return ((63 - ceil_log2(lx * lx * lx)) / 2) < 25 ? ((63 - ceil_log2(lx * lx * lx)) / 2) : 25;
+// max scale-A energy exponent: e_max 2^h in [2^(EM-1), 2^EM), sum of lx^3 < 2^63
+__host__ __device__ constexpr int energy_EM(int lx) {
+  return (63 - ceil_log2(lx * lx * lx)) < 52 ? (63 - ceil_log2(lx * lx * lx)) : 52;
 }
 __host__ __device__ constexpr int linf_K(int lx) { return 63 - ceil_log2(lx * lx * lx); }
 __device__ __forceinline__ uint64_t low52(double t) {
@@ -144,15 +148,33 @@ __device__ __forceinline__ uint64_t low52(double t) {
 __device__ __forceinline__ double pow2d(int e) {  // 2^e for e in [-1022, 1023]
   return __longlong_as_double((long long)(e + 1023) << 52);
 }
-__device__ __forceinline__ uint64_t e_lo(double a, double f) {
-  const double t = __dmul_rn(a, f);
-  return low52(__dadd_rd(__dmul_rn(t, t), 4503599627370496.0));
-}
 __device__ __forceinline__ uint64_t abs_bits(double a) {
   return (uint64_t)__double_as_longlong(a) & 0x7FFFFFFFFFFFFFFFull;
 }
-// strict upper bound of e used for discarded energy: floor(e) + 1
-__device__ __forceinline__ uint64_t e_hi(double a, double f) { return e_lo(a, f) + 1ull; }
+constexpr double kTwo52 = 4503599627370496.0;
+constexpr double kTwo53 = 9007199254740992.0;
+constexpr uint64_t kHiSat = 1ull << 52;  // saturated hi: larger than any threshold
+// scale-B upper bound of the energy of a (already pre-scaled), f = 2^k, sB = 2^(h+G)
+__device__ __forceinline__ uint64_t hi_v2(double a, double f, double sB) {
+  const double x = __dmul_rn(a, f);
+  const double t = __fma_rd(__dmul_rd(x, x), sB, kTwo52);
+  return t < kTwo53 ? low52(t) + 1ull : kHiSat;
+}
+// thr and G from T (scale A) and RD(eps^2) = eps_m 2^eps_e (eps_m < 2^53), h
+__device__ __forceinline__ uint64_t thr_v2(uint64_t T, uint64_t eps_m, int eps_e, int h, int& G) {
+  const uint64_t plo = T * eps_m, phi = __umul64hi(T, eps_m);
+  if ((plo | phi) == 0ull) { G = 0; return 0ull; }
+  const int L = phi ? 128 - __clzll((long long)phi) : 64 - __clzll((long long)plo);
+  int g = 52 - L - eps_e;
+  g = g > 1023 - h ? 1023 - h : g;
+  G = g;
+  const int sh = g + eps_e;  // thr = floor(P 2^sh)
+  if (sh >= 0) return plo << sh;  // L + sh <= 52: P < 2^64 here
+  const int r = -sh;
+  if (r >= 128) return 0ull;
+  if (r >= 64) return phi >> (r - 64);
+  return (plo >> r) | (r ? (phi << (64 - r)) : 0ull);
+}
 // x * 2^e, exact for results in the normal range (cheap common case of ldexp)
 __device__ __forceinline__ double scale2(double x, int e) {
   return (e >= -1022 && e <= 1023) ? __dmul_rn(x, pow2d(e)) : ldexp(x, e);
@@ -246,7 +268,7 @@ struct LaneGroup {
 // ---------------------------------------------------------------------------
 template <int G, class Src>
 __device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const Src& src, int n, uint64_t R,
-                                             double f, unsigned long long* hist, uint64_t& tstar,
+                                             double f, double sB, unsigned long long* hist, uint64_t& tstar,
                                              uint32_t& icut, uint64_t& dsum) {
   uint64_t klo = ~0ull, khi = 0;
   for (int p = g.rank; p < n; p += G) {
@@ -262,7 +284,7 @@ __device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const Src& s
     const uint64_t span = khi - klo;
     if (span == 0) {
       // tie group: every undecided element has key == klo
-      const uint64_t h = e_hi(__longlong_as_double((long long)klo), f);
+      const uint64_t h = hi_v2(__longlong_as_double((long long)klo), f, sB);
       uint32_t cnt = 0;
       for (int p = g.rank; p < n; p += G) { uint64_t k; uint32_t ix; src(p, k, ix); cnt += (k == klo); }
       const uint32_t gcount = g.sum(cnt);
@@ -298,7 +320,7 @@ __device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const Src& s
       uint64_t k; uint32_t ix;
       src(p, k, ix);
       if (k >= klo && k <= khi)
-        atomicAdd(&hist[(k - klo) >> shift], (unsigned long long)e_hi(__longlong_as_double((long long)k), f));
+        atomicAdd(&hist[(k - klo) >> shift], (unsigned long long)hi_v2(__longlong_as_double((long long)k), f, sB));
     }
     g.sync();
     constexpr int BPL = 64 / G;

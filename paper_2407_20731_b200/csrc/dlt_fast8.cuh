@@ -95,7 +95,7 @@ __device__ __forceinline__ uint32_t warp_exscan_u32(uint32_t v, int lane) {
 // (same algorithm as radix_select in dlt_common.cuh, elements in registers).
 // out = {t*, icut, discarded hi-sum}.
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void radix_select16(uint32_t tpark, int lane, uint64_t R, double f, double pre,
+__device__ __noinline__ void radix_select16(uint32_t tpark, int lane, uint64_t R, double f, double sB, double pre,
                                             unsigned long long* hist, uint64_t* out) {
   double v[16];  // the parked coefficients (TMEM); pre: exact tiny-block pre-scale (else 1)
   tmem_wait_st();
@@ -115,7 +115,7 @@ __device__ __noinline__ void radix_select16(uint32_t tpark, int lane, uint64_t R
   for (;;) {
     const uint64_t span = khi - klo;
     if (span == 0) {
-      const uint64_t h = e_lo(__longlong_as_double((long long)klo), f) + 1;
+      const uint64_t h = hi_v2(__longlong_as_double((long long)klo), f, sB);
       uint32_t cnt = 0;
 #pragma unroll
       for (int r = 0; r < 16; ++r) cnt += (abs_bits(v[r]) == klo);
@@ -150,7 +150,7 @@ __device__ __noinline__ void radix_select16(uint32_t tpark, int lane, uint64_t R
     const int bits = 64 - __clzll((long long)span);
     const int shift = bits > 6 ? bits - 6 : 0;
     // 64 bins of energy sums as three 21-bit digit planes of native 32-bit shared
-    // atomics (each value < 2^51, 512 values: every plane sum stays < 2^31)
+    // atomics (each value <= 2^52, 512 values: every plane sum stays < 2^31)
     uint32_t* h32 = reinterpret_cast<uint32_t*>(hist);
 #pragma unroll
     for (int j = 0; j < 6; ++j) h32[lane + 32 * j] = 0u;
@@ -160,7 +160,7 @@ __device__ __noinline__ void radix_select16(uint32_t tpark, int lane, uint64_t R
       const uint64_t k = abs_bits(v[r]);
       if (k >= klo && k <= khi) {
         const uint32_t bin = (uint32_t)((k - klo) >> shift);
-        const uint64_t h = e_lo(v[r], f) + 1ull;
+        const uint64_t h = hi_v2(v[r], f, sB);
         atomicAdd(&h32[bin], (uint32_t)(h & 0x1FFFFFu));
         atomicAdd(&h32[64 + bin], (uint32_t)((h >> 21) & 0x1FFFFFu));
         atomicAdd(&h32[128 + bin], (uint32_t)(h >> 42));
@@ -229,7 +229,7 @@ __device__ unsigned long long g_pathstats[16];
 // smem: bins = 3 x 256 u32, cand = 32 u64.
 // ---------------------------------------------------------------------------
 constexpr int kSelBins = 256;
-__device__ __noinline__ bool select_bins16(uint32_t tpark, int lane, uint64_t R, double f, double pre,
+__device__ __noinline__ bool select_bins16(uint32_t tpark, int lane, uint64_t R, double f, double sB, double pre,
                                            uint32_t* bins, uint64_t* cand, uint64_t* out) {
   uint64_t kk[16], hv[16];
   uint32_t bn[16];
@@ -241,7 +241,7 @@ __device__ __noinline__ bool select_bins16(uint32_t tpark, int lane, uint64_t R,
     for (int r = 0; r < 16; ++r) {
       const double a = __dmul_rn(v[r], pre);
       kk[r] = abs_bits(a);
-      hv[r] = e_lo(a, f) + 1ull;  // in [1, 2^51)
+      hv[r] = hi_v2(a, f, sB);  // in [1, 2^52]
     }
     // bins: quarter binades of |a| (exponent and the next two bits: kk >> 50, a
     // monotone function of the key) counted down from the block maximum; the lowest
@@ -330,7 +330,7 @@ __device__ __noinline__ bool select_bins16(uint32_t tpark, int lane, uint64_t R,
       const bool lower = ((lane & j) == 0);
       key = (lower == up) ? (o < key ? o : key) : (o > key ? o : key);
     }
-  const uint64_t h = lane < (int)ncand ? e_lo(__longlong_as_double((long long)key), f) + 1ull : 0ull;
+  const uint64_t h = lane < (int)ncand ? hi_v2(__longlong_as_double((long long)key), f, sB) : 0ull;
   uint64_t cs = h;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -371,37 +371,48 @@ __device__ __noinline__ bool select_bins16(uint32_t tpark, int lane, uint64_t R,
 
 struct Sel16 {
   uint32_t mask;   // kept bits of this lane's 16 coefficients
-  uint64_t T;      // block total of lo energies
-  uint64_t hdisc;  // block hi-sum of the discarded set
-  int k;           // energy scale exponent (e = a^2 * 2^(2k))
+  uint64_t T;      // block total at scale A (rule v2)
+  uint64_t hdisc;  // hi-sum of the discarded set at scale B
+  int eT, eD;      // energy = T 2^eT = hdisc 2^eD
   bool nonfinite;
 };
+
+// sqrt(2) - 1 in units of 2^-20, floor: the 20 leading fraction bits of max|a| decide
+// whether its energy lies below 2^51 (h = 1) except for this one value
+constexpr uint32_t kSqrt2F20 = 434334u;
 
 // v[r] = coefficient 16*lane + r of the warp's block (consumed: only pass 0/1 read
 // it); tpark = the same coefficients parked in tensor memory (32x32b, lane = thread,
 // columns 2r, 2r+1), re-read by the one-move and general paths and by the encoder.
-__device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t eps_q, unsigned long long* hist,
-                                          uint32_t tpark) {
-  Sel16 s{0u, 0ull, 0ull, 0, false};
+// Truncation rule v2 (oracle/isf_oracle.c select_impl).
+__device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t eps_m, int eps_e,
+                                          unsigned long long* hist, uint32_t tpark) {
+  Sel16 s{0u, 0ull, 0ull, 0, 0, false};
   uint32_t hm = 0;
 #pragma unroll
   for (int r = 0; r < 16; ++r) hm = ::max(hm, (uint32_t)__double2hiint(v[r]) & 0x7fffffffu);
   hm = __reduce_max_sync(0xffffffffu, hm);
   if (hm >= 0x7ff00000u) { s.nonfinite = true; return s; }
-  int sexp;
-  if (hm >= 0x00100000u) {
+  constexpr int EM = energy_EM(8), HM = EM / 2;  // 52, 26
+  int sexp, h;
+  const uint32_t f20 = hm & 0xFFFFFu;
+  if (hm >= 0x00100000u && f20 != kSqrt2F20) {
     sexp = (int)(hm >> 20) - 1022;
-  } else {  // subnormal maximum or all-zero block (rare)
+    h = f20 < kSqrt2F20 ? 1 : 0;  // max energy (m 2^25)^2 < 2^51  <=>  m < sqrt 2
+  } else {  // subnormal maximum, all-zero block, or the undecided leading bits (rare)
     uint64_t mb = 0;
 #pragma unroll
     for (int r = 0; r < 16; ++r) { const uint64_t b = abs_bits(v[r]); mb = b > mb ? b : mb; }
     mb = warp_max_u64(mb);
     if (mb == 0) return s;  // all-zero block keeps nothing
-    sexp = 64 - __clzll((long long)mb) - 1074;
+    sexp = hm >= 0x00100000u ? (int)(hm >> 20) - 1022 : 64 - __clzll((long long)mb) - 1074;
+    const int kk = HM - sexp;
+    const double am = __longlong_as_double((long long)mb);
+    const double xm = kk > 1023 ? __dmul_rn(__dmul_rn(am, pow2d(kk - 1023)), pow2d(1023)) : __dmul_rn(am, pow2d(kk));
+    h = (EM - 2 * HM) + (__dmul_rd(xm, xm) < pow2d(2 * HM - 1) ? 1 : 0);
   }
-  constexpr int K = energy_K(8);
-  int k = K - sexp;
-  s.k = k;
+  int k = HM - sexp;
+  const int k0 = k;
   // |a| < 2^-998: exact pre-scale by 2^(k-1023) (applied to every read below)
   const double pre = k > 1023 ? pow2d(k - 1023) : 1.0;
   if (k > 1023) {
@@ -410,35 +421,42 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
     k = 1023;
   }
   const double f = pow2d(k);
-  // t_r = 2^52 + floor(e_r) exactly (round-down add); its bit pattern is C + lo_r
+  const double sA = h ? 2.0 : 1.0;
+  // e_r = RD(x_r^2); scale A: 2^52 + floor(e_r 2^h) exactly (round-down fma), its bit
+  // pattern is C52 + floor(e_r 2^h)
   constexpr uint64_t C52 = 0x4330000000000000ull;
   double t[16];
   uint64_t t0 = 0, t1 = 0;
 #pragma unroll
   for (int r = 0; r < 16; r += 2) {
     const double xa = __dmul_rn(v[r], f), xb = __dmul_rn(v[r + 1], f);
-    t[r] = __dadd_rd(__dmul_rn(xa, xa), 4503599627370496.0);
-    t[r + 1] = __dadd_rd(__dmul_rn(xb, xb), 4503599627370496.0);
-    t0 += (uint64_t)__double_as_longlong(t[r]);
-    t1 += (uint64_t)__double_as_longlong(t[r + 1]);
+    t[r] = __dmul_rd(xa, xa);
+    t[r + 1] = __dmul_rd(xb, xb);
+    t0 += (uint64_t)__double_as_longlong(__fma_rd(t[r], sA, kTwo52));
+    t1 += (uint64_t)__double_as_longlong(__fma_rd(t[r + 1], sA, kTwo52));
   }
   const uint64_t T = warp_sum_u58(t0 + t1 - 16 * C52);
   s.T = T;
-  const uint64_t thr = __umul64hi(T, eps_q);
+  int G;
+  const uint64_t thr = thr_v2(T, eps_m, eps_e, h, G);
+  s.eT = -2 * k0 - h;
+  s.eD = -2 * k0 - h - G;
+  const double sB = pow2d(h + G);
+  // scale B: t_r = 2^52 + floor(e_r 2^(h+G)) (>= 2^53: saturated, never discardable)
+#pragma unroll
+  for (int r = 0; r < 16; ++r) t[r] = __fma_rd(t[r], sB, kTwo52);
   // kept-above-threshold set H: hi = lo + 1 > thr  <=>  lo >= thr  <=>  t >= 2^52 + thr
-  // 2^52 + min(thr, 2^51) exactly, from its bit pattern (no integer -> fp64 conversion)
-  const double tthr = __longlong_as_double((long long)(C52 + (thr < (1ull << 51) ? thr : (1ull << 51))));
+  const double tthr = __longlong_as_double((long long)(C52 + thr));  // thr < 2^52
   uint32_t mH = 0;
-  uint64_t h0 = 0, h1s = 0;
+  uint64_t n0 = 0, n1 = 0;
 #pragma unroll
   for (int r = 0; r < 16; r += 2) {
-    if (t[r] >= tthr) { mH |= 1u << r; h0 += (uint64_t)__double_as_longlong(t[r]); }
-    if (t[r + 1] >= tthr) { mH |= 1u << (r + 1); h1s += (uint64_t)__double_as_longlong(t[r + 1]); }
+    if (t[r] >= tthr) mH |= 1u << r; else n0 += (uint64_t)__double_as_longlong(t[r]);
+    if (t[r + 1] >= tthr) mH |= 1u << (r + 1); else n1 += (uint64_t)__double_as_longlong(t[r + 1]);
   }
-  const uint32_t nH = (uint32_t)__popc(mH);
-  const uint64_t SH = warp_sum_u58(h0 + h1s - nH * C52);  // sum of lo over H
-  const uint32_t NH = __reduce_add_sync(0xffffffffu, nH);
-  const uint64_t SN = T - SH + (512u - NH);                  // sum of hi over the rest
+  const uint32_t nN = 16u - (uint32_t)__popc(mH);
+  // sum of hi = lo + 1 over the rest (each lo < thr < 2^52: per-lane sum < 2^56)
+  const uint64_t SN = warp_sum_u58(n0 + n1 - nN * C52 + nN);
   if (SN <= thr) {
     ISF_PATH(1);
     s.mask = mH;
@@ -499,9 +517,9 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
     }
   }
   uint64_t res[3];
-  if (!select_bins16(tpark, lane, thr, f, pre, reinterpret_cast<uint32_t*>(hist) + 64,
+  if (!select_bins16(tpark, lane, thr, f, sB, pre, reinterpret_cast<uint32_t*>(hist) + 64,
                      reinterpret_cast<uint64_t*>(hist), res))
-    radix_select16(tpark, lane, thr, f, pre, hist, res);
+    radix_select16(tpark, lane, thr, f, sB, pre, hist, res);
   const uint64_t tstar = res[0];
   const uint32_t icut = (uint32_t)res[1];
   uint32_t mk2 = 0;
@@ -755,7 +773,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     Sel16 sel{0u, 1ull, 0ull, 0, false};
     if (__double_as_longlong(v[0]) == 0x1234) sel.mask = 1;
 #else
-    const Sel16 sel = select16(v, lane, A.eps_q, hist, tpark);
+    const Sel16 sel = select16(v, lane, A.eps_m, A.eps_e, hist, tpark);
 #endif
     if (sel.nonfinite && lane == 0) atomicOr(A.ws.flags, kFlagNonFinite);
     mask = sel.nonfinite ? 0u : sel.mask;
@@ -796,14 +814,12 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       }
     }
     if (!sel.nonfinite && sel.T) {
-      const int e2 = -2 * sel.k;
-      if (e2 >= -1022 && e2 <= 1023) {  // the usual case: one exact power-of-two scale
-        const double sc = pow2d(e2);
-        tot_acc = __fma_rn((double)sel.T, sc, tot_acc);
-        disc_acc = __fma_rn((double)sel.hdisc, sc, disc_acc);
+      if (sel.eT >= -1022 && sel.eT <= 1023 && sel.eD >= -1022 && sel.eD <= 1023) {  // exact power-of-two scales
+        tot_acc = __fma_rn((double)sel.T, pow2d(sel.eT), tot_acc);
+        disc_acc = __fma_rn((double)sel.hdisc, pow2d(sel.eD), disc_acc);
       } else {
-        tot_acc += ldexp((double)sel.T, e2);
-        disc_acc += ldexp((double)sel.hdisc, e2);
+        tot_acc += ldexp((double)sel.T, sel.eT);
+        disc_acc += ldexp((double)sel.hdisc, sel.eD);
       }
     }
     (void)off;

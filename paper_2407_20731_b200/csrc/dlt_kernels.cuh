@@ -29,7 +29,8 @@ struct CompressArgs {
   uint64_t cap;
   uint64_t mask_off;  // byte offset of masks
   uint64_t val_off;   // byte offset of values
-  uint64_t eps_q;     // floor(eps^2 * 2^64)
+  uint64_t eps_m;     // RD(eps^2) = eps_m * 2^eps_e, eps_m < 2^53 (truncation rule v2)
+  int eps_e;
   double eps;         // max_error (RelativeLInf budget)
   int norm;           // ISF_NORM_RELATIVE_L2 (0) or ISF_NORM_RELATIVE_LINF (1; generic kernels)
   double* vslot;      // lx=8 fast path: per-tile value slots (2048 doubles per tile)
@@ -129,16 +130,16 @@ struct GenDSmem {
 
 // selection on warp 0 over the coefficients in smem u[]
 template <int LX>
-__device__ void select_generic(double* u, uint64_t eps_q, uint16_t* cidx,
+__device__ void select_generic(double* u, uint64_t eps_m, int eps_e, uint16_t* cidx,
                                unsigned long long* hist, uint64_t* maskw, uint64_t& T_out,
-                               uint64_t& hdisc_out, int& k_out, bool& nonfinite) {
+                               uint64_t& hdisc_out, int& eT_out, int& eD_out, bool& nonfinite) {
   constexpr int N3 = LX * LX * LX;
   constexpr int W = (N3 + 63) / 64;
   constexpr int NR = (N3 + 31) / 32;
   const LaneGroup<32> g;
   const int lane = g.rank;
   for (int w = lane; w < 64; w += 32) maskw[w] = 0ull;
-  T_out = 0; hdisc_out = 0; k_out = 0; nonfinite = false;
+  T_out = 0; hdisc_out = 0; eT_out = 0; eD_out = 0; nonfinite = false;
   uint64_t mb = 0;
   for (int p = lane; p < N3; p += 32) { const uint64_t b = abs_bits(u[p]); mb = b > mb ? b : mb; }
   mb = g.max(mb);
@@ -150,9 +151,9 @@ __device__ void select_generic(double* u, uint64_t eps_q, uint16_t* cidx,
     const uint32_t hm = (uint32_t)(mb >> 32);
     s = hm >= 0x00100000u ? (int)(hm >> 20) - 1022 : 64 - __clzll((long long)mb) - 1074;
   }
-  constexpr int K = energy_K(LX);
-  int k = K - s;
-  k_out = k;
+  constexpr int EM = energy_EM(LX), HM = EM / 2;
+  int k = HM - s;
+  const int k0 = k;
   const bool tiny = k > 1023;
   if (tiny) {
     const double pre = pow2d(k - 1023);
@@ -160,11 +161,26 @@ __device__ void select_generic(double* u, uint64_t eps_q, uint16_t* cidx,
     k = 1023;
   }
   const double f = pow2d(k);
+  // h from the largest energy (the key maximum): e_max 2^h in [2^(EM-1), 2^EM)
+  int h;
+  {
+    const double xm = __dmul_rn(__longlong_as_double((long long)mb), tiny ? pow2d(k0 - 1023) : 1.0);
+    const double xs = __dmul_rn(xm, f);
+    h = (EM - 2 * HM) + (__dmul_rd(xs, xs) < pow2d(2 * HM - 1) ? 1 : 0);
+  }
+  const double sA = pow2d(h);
   uint64_t T = 0;
-  for (int p = lane; p < N3; p += 32) T += e_lo(u[p], f);
+  for (int p = lane; p < N3; p += 32) {
+    const double x = __dmul_rn(u[p], f);
+    T += low52(__fma_rd(__dmul_rd(x, x), sA, kTwo52));
+  }
   T = g.sum(T);
   T_out = T;
-  const uint64_t thr = __umul64hi(T, eps_q);
+  int G;
+  const uint64_t thr = thr_v2(T, eps_m, eps_e, h, G);
+  const double sB = pow2d(h + G);
+  eT_out = -2 * k0 - h;
+  eD_out = -2 * k0 - h - G;
   // one pass: the sure-kept mask (e > thr), the discardable sum SN, and, in case SN
   // exceeds the budget, the sure-discarded sum SL (e <= thr / N3) with the candidates
   // in between compacted by index for the radix select
@@ -175,7 +191,7 @@ __device__ void select_generic(double* u, uint64_t eps_q, uint16_t* cidx,
     const int p = r * 32 + lane;
     bool sure = false, cand = false;
     if (p < N3) {
-      const uint64_t h = e_hi(u[p], f);
+      const uint64_t h = hi_v2(u[p], f, sB);
       sure = h > thr;
       if (!sure) {
         SN += h;
@@ -196,9 +212,9 @@ __device__ void select_generic(double* u, uint64_t eps_q, uint16_t* cidx,
     __syncwarp();
     uint64_t tstar, dsum;
     uint32_t icut;
-    radix_select<32>(g, SrcIndirect{u, cidx}, (int)base, thr - SL, f, hist, tstar, icut, dsum);
+    radix_select<32>(g, SrcIndirect{u, cidx}, (int)base, thr - SL, f, sB, hist, tstar, icut, dsum);
     // the cut (tstar, icut) is a candidate key (>= 1 candidate here, since SL <= thr < SN)
-    // and e_hi is monotone in |a|: sure-discarded coefficients lie strictly below it, sure-
+    // and hi_v2 is monotone in |a|: sure-discarded coefficients lie strictly below it, sure-
     // kept ones above, so the key comparison alone decides every coefficient
     for (int r = 0; r < NR; ++r) {
       const int p = r * 32 + lane;
@@ -213,7 +229,7 @@ __device__ void select_generic(double* u, uint64_t eps_q, uint16_t* cidx,
     hdisc_out = SL + dsum;
   }
   if (tiny) {
-    const double un = pow2d(1023 - k_out);
+    const double un = pow2d(1023 - k0);
     for (int p = lane; p < N3; p += 32) u[p] = __dmul_rn(u[p], un);
   }
   (void)W;
@@ -331,14 +347,14 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
     __syncthreads();
     if (kGenCThreads == 32 || warp == 0) {  // single-warp CTA: no divergent region
       uint64_t T, hd;
-      int k;
+      int eT, eD;
       bool nf;
       if (A.norm) {
         select_linf<LX>(u, __longlong_as_double((long long)misc[3]), A.eps, hist, maskw, nf);
         T = hd = 0;
-        k = 0;
+        eT = eD = 0;
       } else {
-        select_generic<LX>(u, A.eps_q, cidx, hist, maskw, T, hd, k, nf);
+        select_generic<LX>(u, A.eps_m, A.eps_e, cidx, hist, maskw, T, hd, eT, eD, nf);
       }
       if (nf) {
         for (int w = lane; w < W; w += 32) maskw[w] = 0ull;
@@ -355,8 +371,8 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
       if (lane == 0) {
         counts[blk] = nk;
         if (blk + 1 == A.nblocks) for (uint64_t pb = A.nblocks; pb < ((A.nblocks + 3) & ~3ull); ++pb) counts[pb] = 0;
-        A.ws.partials[blk * 4 + 0] = nf ? 0.0 : ldexp((double)T, -2 * k);
-        A.ws.partials[blk * 4 + 1] = nf ? 0.0 : ldexp((double)hd, -2 * k);
+        A.ws.partials[blk * 4 + 0] = nf ? 0.0 : ldexp((double)T, eT);
+        A.ws.partials[blk * 4 + 1] = nf ? 0.0 : ldexp((double)hd, eD);
       }
       for (int w = lane; w < W; w += 32) masks[blk * W + w] = maskw[w];
     }

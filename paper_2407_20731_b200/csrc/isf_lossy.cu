@@ -272,9 +272,22 @@ int check_plan(const isf_lossy_plan* p) {
   return 0;
 }
 
-uint64_t eps_q_of(double max_error) {
-  const double e2 = max_error * max_error;
-  return (uint64_t)ldexp(e2, 64);
+// RD(eps^2) = m 2^e with m < 2^53 an integer (truncation rule v2): the
+// exact square is p + err (err = fma(eps, eps, -p)); round down when err < 0.  Near the
+// subnormal range the fma error is not exact, so binary128 decides there.
+void eps2_rd(double max_error, uint64_t& m, int& e) {
+  double p = max_error * max_error;
+  if (p < 0x1p-960) {
+    const __float128 q = (__float128)max_error * (__float128)max_error;
+    p = (double)q;
+    if ((__float128)p > q) p = std::nextafter(p, 0.0);
+  } else if (std::fma(max_error, max_error, -p) < 0.0) {
+    p = std::nextafter(p, 0.0);
+  }
+  int ex = 0;
+  const double fr = std::frexp(p, &ex);
+  m = (uint64_t)std::ldexp(fr, 53);
+  e = ex - 53;
 }
 
 }  // namespace
@@ -433,7 +446,7 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   a.cap = capacity;
   a.mask_off = (4 * B + 15) & ~15ull;
   a.val_off = hdr;
-  a.eps_q = eps_q_of(max_error);
+  eps2_rd(max_error, a.eps_m, a.eps_e);
   a.eps = max_error;
   a.norm = error_norm;
   a.vslot = nullptr;

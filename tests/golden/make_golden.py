@@ -10,9 +10,10 @@ definitions in DESIGN.md 3 (SPEC.md:222-239 + north_star's Legendre DLT):
     first product then ascending fused multiply-adds), every fma evaluated
     exactly with `fractions.Fraction` and rounded once (float(Fraction) is
     correctly rounded), so the coefficients are bit-exact by construction;
-  * the truncation rule with Python integers and an explicit stable sort
-    (|a| descending, index ascending: "sort coefficients by
-    magnitude descending ... smallest prefix");
+  * the truncation rule (v2: exact integer energies at a block-total scale and
+    a threshold-relative scale) with Python integers / fractions and an explicit
+    stable sort (|a| descending, index ascending: "sort coefficients
+    by magnitude descending ... smallest prefix");
   * the little-endian stream layout of include/isf_lossy.h.
 
 The reference (/root/reference) has no implementation and no test vectors for
@@ -162,28 +163,47 @@ def fwd_block(F, u, n):
 
 
 # ------------------------------------------------------------ truncation rule
+def _rd(q: Fraction) -> float:
+    """Largest binary64 <= q (q >= 0, finite)."""
+    f = float(q)  # correctly rounded to nearest
+    if Fraction(f) > q:
+        f = math.nextafter(f, 0.0)
+    return f
+
+
 def select(a, n3, eps):
-    K = min(25, (63 - math.ceil(math.log2(n3))) // 2)
+    """Rule v2 of DESIGN.md 3.4 (two integer scales) with Python integers."""
+    EM = min(52, 63 - math.ceil(math.log2(n3)))
+    hm = EM // 2
     bits = [struct.unpack("<Q", struct.pack("<d", float(abs(x))))[0] for x in a]
     if max(bits) == 0:
         return [False] * n3
     _, s = math.frexp(max(abs(x) for x in a))
-    k = K - s
-    lo = []
-    for x in a:
-        sx = math.ldexp(abs(x), k)
-        lo.append(int(math.floor(sx * sx)))
-    T = sum(lo)
-    q = int(math.ldexp(eps * eps, 64))
-    thr = (T * q) >> 64
+    k = hm - s
+    e = [_rd(Fraction(math.ldexp(abs(x), k)) ** 2) for x in a]   # RD(x^2), x exact
+    h = (EM - 2 * hm) + (1 if max(e) < 2.0 ** (2 * hm - 1) else 0)
+    T = sum(int(Fraction(v) * 2 ** h) for v in e)                  # floor: values >= 0
+    E2 = _rd(Fraction(eps) ** 2)
+    m, ex = math.frexp(E2)
+    M, Ee = int(math.ldexp(m, 53)), ex - 53
+    P = T * M
+    if P == 0:
+        thr, G = 0, 0
+    else:
+        G = min(52 - P.bit_length() - Ee, 1023 - h)
+        sh = G + Ee
+        thr = P << sh if sh >= 0 else P >> (-sh)
+    def hi(v):
+        y = Fraction(v) * Fraction(2) ** (h + G)
+        return 2 ** 52 if y >= 2 ** 52 else int(y) + 1
     order = sorted(range(n3), key=lambda j: (-bits[j], j))   # |a| desc, index asc (stable)
     disc = order[::-1]                                       # discard order
-    acc, m = 0, 0
-    while m < n3 and acc + lo[disc[m]] + 1 <= thr:
-        acc += lo[disc[m]] + 1
-        m += 1
+    acc, mm = 0, 0
+    while mm < n3 and acc + hi(e[disc[mm]]) <= thr:
+        acc += hi(e[disc[mm]])
+        mm += 1
     kept = [True] * n3
-    for j in disc[:m]:
+    for j in disc[:mm]:
         kept[j] = False
     return kept
 
@@ -278,8 +298,8 @@ def main():
         out[f"{name}__meta"] = np.array([lx, eps])
         names.append(name)
     out["cases"] = np.array(names)
-    np.savez_compressed(os.path.join(HERE, "golden_v1.npz"), **out)
-    print("wrote", os.path.join(HERE, "golden_v1.npz"), names)
+    np.savez_compressed(os.path.join(HERE, "golden_v2.npz"), **out)
+    print("wrote", os.path.join(HERE, "golden_v2.npz"), names)
 
 
 if __name__ == "__main__":

@@ -477,36 +477,3 @@ def test_generic_large_sampled_parity(native, oracle, P):
         rc_, rm, rv = oracle.parse_stream(ref, P, S)
         assert np.array_equal(gc[b0:b0 + S], rc_) and np.array_equal(gm[b0:b0 + S], rm)
         assert np.array_equal(np.asarray(gv[go[b0]:go[b0 + S]]).view(np.uint64), np.asarray(rv).view(np.uint64))
-
-
-@pytest.mark.parametrize("which", [0, 3])
-def test_cfg2_full_size_sampled_parity(native, oracle, which):
-    """cfg2 at full size (64^3 elements of lx = 8, 1 GiB per field) on the fast path:
-    deterministic streams, the L2 bound, and three 128-block windows of the stream
-    (counts, masks, value records) bit-identical to the oracle run on the same input
-    blocks (offsets and compaction at full size)."""
-    import paper_2407_20731_b200 as PK
-    E, P, S = 64, 8, 128
-    n = E ** 3
-    plan = PK.get_plan(P, 1, 0)
-    vals = torch.empty(n * 512, dtype=torch.float64, device="cuda")
-    plan.generate_tgv(vals, E, which)
-    f = PK.Field(E, P, 1, vals)
-    eps = 1e-3
-    a = PK.lossy_compress(f, PK.LossyConfig(eps))
-    b = PK.lossy_compress(f, PK.LossyConfig(eps))
-    assert torch.equal(a.stream, b.stream)
-    back, rep = PK.decompress_with_error(a, f.shape, f)
-    assert 0 < rep.rel_l2 <= eps * (1 + 1e-9)
-    got = a.stream.cpu().numpy()
-    gc, gm, gv = oracle.parse_stream(got, P, n)
-    go = np.concatenate([[0], np.cumsum(gc.astype(np.int64))])
-    for b0 in (0, n // 2 + 77, n - S):
-        u = vals[b0 * 512:(b0 + S) * 512].cpu().numpy()
-        rc, ref, _ = oracle.compress(u, P, 1, eps)
-        assert rc == 0
-        rc_, rm, rv = oracle.parse_stream(ref, P, S)
-        assert np.array_equal(gc[b0:b0 + S], rc_) and np.array_equal(gm[b0:b0 + S], rm)
-        assert np.array_equal(np.asarray(gv[go[b0]:go[b0 + S]]).view(np.uint64), np.asarray(rv).view(np.uint64))
-        rc, ob, _ = oracle.decompress(ref, P, 1, S)
-        assert np.array_equal(back.values[b0 * 512:(b0 + S) * 512].cpu().numpy().view(np.uint64), ob.view(np.uint64))
