@@ -138,6 +138,11 @@ int isf_lossy_decompress_host(isf_lossy_plan* plan, const void* h_stream, uint64
  * NCCL is resolved at run time from the process (dlsym), so the library has no
  * link-time NCCL dependency and uses whichever NCCL created the communicator. */
 int isf_lossy_allreduce(isf_lossy_stats* d_stats, void* nccl_comm, void* cuda_stream);
+/* The same over n consecutive records d_stats[0..n) (1 <= n <= 256, e.g. the four
+ * fields of a step) in one NCCL group: three all-reduces whatever n is.  The NCCL
+ * symbols come from the libnccl instance already loaded in the process (the one that
+ * created the communicator), else from the global scope. */
+int isf_lossy_allreduce_n(isf_lossy_stats* d_stats, uint32_t n, void* nccl_comm, void* cuda_stream);
 
 /* Device CRC-32 (IEEE / zlib polynomial; replaces the host zlib call of
  * proj/src/core/crc32.cpp:7-20 for device-resident data): *d_crc = crc32(d_data[0..n)).

@@ -14,7 +14,8 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "_build", "libisf_oracle.so")
+# ISF_ORACLE_LIB: the -O3 -march=native build made on the benchmark host (bench.py)
+_LIB_PATH = os.environ.get("ISF_ORACLE_LIB") or os.path.join(_HERE, "_build", "libisf_oracle.so")
 
 
 class Stats(ctypes.Structure):
@@ -32,6 +33,8 @@ class Stats(ctypes.Structure):
 
 
 def build(force: bool = False) -> str:
+    if os.environ.get("ISF_ORACLE_LIB"):
+        return _LIB_PATH
     if force or not os.path.exists(_LIB_PATH) or (
         os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "isf_oracle.c"))
     ):

@@ -18,7 +18,7 @@ EXPORTS = (
     "isf_lossy_plan_create", "isf_lossy_plan_destroy", "isf_lossy_stream_capacity",
     "isf_lossy_stream_header_bytes", "isf_lossy_compress_async", "isf_lossy_compress",
     "isf_lossy_decompress_async", "isf_lossy_decompress", "isf_lossy_compress_host",
-    "isf_lossy_decompress_host", "isf_lossy_allreduce", "isf_lossy_compression_ratio",
+    "isf_lossy_decompress_host", "isf_lossy_allreduce", "isf_lossy_allreduce_n", "isf_lossy_compression_ratio",
     "isf_lossy_last_error", "isf_lossy_error_code_name", "isf_lossy_plan_operators",
     "isf_lossy_plan_last_launches", "isf_lossy_plan_set_compress_mode", "isf_lossy_generate_tgv", "isf_lossy_generate_spectral",
     "isf_lossy_solver_standin", "isf_lossy_crc32", "isf_lossy_frame_async",
@@ -66,6 +66,7 @@ def lib() -> ctypes.CDLL:
         "isf_lossy_compress_host": ([P, P, u64, f64, i32, P, u64, ctypes.POINTER(u64), Sp], i32),
         "isf_lossy_decompress_host": ([P, P, u64, u64, P, P, Sp], i32),
         "isf_lossy_allreduce": ([P, P, P], i32),
+        "isf_lossy_allreduce_n": ([P, u32, P, P], i32),
         "isf_lossy_compression_ratio": ([u64, u64], f64),
         "isf_lossy_last_error": ([], ctypes.c_char_p),
         "isf_lossy_error_code_name": ([i32], ctypes.c_char_p),

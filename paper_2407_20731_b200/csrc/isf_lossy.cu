@@ -783,56 +783,106 @@ int isf_lossy_frame_async(isf_lossy_plan* p, void* d_frame, uint64_t frame_cap, 
 }  // extern "C"
 
 namespace {
-__global__ void status_lanes_kernel(uint64_t* st, int fold) {
-  const uint64_t v = *st;
-  uint64_t r = 0;
-  for (int k = 0; k < 4; ++k) {
-    if (fold) r |= (((v >> (16 * k)) & 0xFFFFull) != 0) ? (1ull << k) : 0ull;
-    else r |= ((v >> k) & 1ull) << (16 * k);
+// isf_lossy_allreduce_n: the n records [n][12] are re-laid out in place as
+//   [sum f64: err2 nrm2 disc2 tot2 x n | max f64: err_inf u_inf x n |
+//    sum u64: kept blocks stream field status-lanes x n | unused x n]
+// so one NCCL group of three all-reduces covers every record.  status is a bit set
+// and NCCL has no OR: bit k is spread into 16-bit lane k, summed, and every non-zero
+// lane folded back to its bit (exact for < 65536 ranks).
+constexpr uint32_t kMaxReduceRecords = 256;
+__global__ void stats_pack_kernel(uint64_t* st, uint32_t n, int unpack) {
+  __shared__ uint64_t t[kMaxReduceRecords * 12];
+  for (uint32_t i = threadIdx.x; i < 12 * n; i += blockDim.x) t[i] = st[i];
+  __syncthreads();
+  for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+    uint64_t* sf = st;            // 4n
+    uint64_t* mf = st + 4 * n;    // 2n
+    uint64_t* su = st + 6 * n;    // 5n
+    if (!unpack) {
+      const uint64_t* x = t + 12 * r;
+      sf[4 * r + 0] = x[0]; sf[4 * r + 1] = x[1]; sf[4 * r + 2] = x[4]; sf[4 * r + 3] = x[5];
+      mf[2 * r + 0] = x[2]; mf[2 * r + 1] = x[3];
+      for (int k = 0; k < 4; ++k) su[5 * r + k] = x[6 + k];
+      uint64_t lanes = 0;
+      for (int k = 0; k < 4; ++k) lanes |= ((x[10] >> k) & 1ull) << (16 * k);
+      su[5 * r + 4] = lanes;
+      st[11 * n + r] = x[11];
+    } else {
+      uint64_t y[12];
+      const uint64_t* tf = t;
+      const uint64_t* tm = t + 4 * n;
+      const uint64_t* tu = t + 6 * n;
+      y[0] = tf[4 * r]; y[1] = tf[4 * r + 1]; y[4] = tf[4 * r + 2]; y[5] = tf[4 * r + 3];
+      y[2] = tm[2 * r]; y[3] = tm[2 * r + 1];
+      for (int k = 0; k < 4; ++k) y[6 + k] = tu[5 * r + k];
+      uint64_t bits = 0;
+      for (int k = 0; k < 4; ++k) bits |= (((tu[5 * r + 4] >> (16 * k)) & 0xFFFFull) != 0) ? (1ull << k) : 0ull;
+      y[10] = bits;
+      y[11] = t[11 * n + r];
+      for (int k = 0; k < 12; ++k) st[12 * r + k] = y[k];
+    }
   }
-  *st = r;
 }
 }  // namespace
 
 typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
 typedef int (*nccl_group_fn)(void);
 
-int isf_lossy_allreduce(isf_lossy_stats* d_stats, void* comm, void* cuda_stream) {
-  if (!d_stats || !comm) return fail(ISF_E_INVALID_ARGUMENT, "null stats or communicator");
-  static nccl_allreduce_fn ar = nullptr;
-  static nccl_group_fn gs = nullptr, ge = nullptr;
-  if (!ar) {
-    ar = (nccl_allreduce_fn)dlsym(RTLD_DEFAULT, "ncclAllReduce");
-    gs = (nccl_group_fn)dlsym(RTLD_DEFAULT, "ncclGroupStart");
-    ge = (nccl_group_fn)dlsym(RTLD_DEFAULT, "ncclGroupEnd");
-    if (!ar) {
-      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+namespace {
+struct NcclSyms {
+  nccl_allreduce_fn ar = nullptr;
+  nccl_group_fn gs = nullptr, ge = nullptr;
+};
+// The communicator belongs to the NCCL instance that created it (e.g. the one torch
+// loaded): prefer an already-loaded libnccl (RTLD_NOLOAD), then the global scope, and
+// only then load one.  Resolved once (thread safe).
+const NcclSyms& nccl_syms() {
+  static NcclSyms s;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_NOLOAD);
+    void* src = h ? h : RTLD_DEFAULT;
+    s.ar = (nccl_allreduce_fn)dlsym(src, "ncclAllReduce");
+    s.gs = (nccl_group_fn)dlsym(src, "ncclGroupStart");
+    s.ge = (nccl_group_fn)dlsym(src, "ncclGroupEnd");
+    if (!s.ar || !s.gs || !s.ge) {
+      h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
       if (h) {
-        ar = (nccl_allreduce_fn)dlsym(h, "ncclAllReduce");
-        gs = (nccl_group_fn)dlsym(h, "ncclGroupStart");
-        ge = (nccl_group_fn)dlsym(h, "ncclGroupEnd");
+        s.ar = (nccl_allreduce_fn)dlsym(h, "ncclAllReduce");
+        s.gs = (nccl_group_fn)dlsym(h, "ncclGroupStart");
+        s.ge = (nccl_group_fn)dlsym(h, "ncclGroupEnd");
       }
     }
-    if (!ar || !gs || !ge) return fail(ISF_E_TASK_FAILED, "NCCL not found in the process");
-  }
+  });
+  return s;
+}
+}  // namespace
+
+int isf_lossy_allreduce_n(isf_lossy_stats* d_stats, uint32_t n, void* comm, void* cuda_stream) {
+  if (!d_stats || !comm) return fail(ISF_E_INVALID_ARGUMENT, "null stats or communicator");
+  if (n == 0 || n > kMaxReduceRecords) return fail(ISF_E_INVALID_ARGUMENT, "record count %u not in [1, %u]", n, kMaxReduceRecords);
+  const NcclSyms& N = nccl_syms();
+  if (!N.ar || !N.gs || !N.ge) return fail(ISF_E_TASK_FAILED, "NCCL not found in the process");
   // ncclDataType_t: ncclUint64 = 5, ncclFloat64 = 8; ncclRedOp_t: ncclSum = 0, ncclMax = 2
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  double* d = reinterpret_cast<double*>(d_stats);
   uint64_t* u = reinterpret_cast<uint64_t*>(d_stats);
-  // status is a bit set and NCCL has no OR: spread bit k into 16-bit lane k, sum,
-  // then fold every non-zero lane back to its bit (exact for < 65536 ranks)
-  status_lanes_kernel<<<1, 1, 0, s>>>(u + 10, 0);
-  int r = gs();
-  r |= ar(d + 0, d + 0, 2, 8, 0, comm, s);   // err2, nrm2
-  r |= ar(d + 2, d + 2, 2, 8, 2, comm, s);   // err_inf, u_inf
-  r |= ar(d + 4, d + 4, 2, 8, 0, comm, s);   // disc2, tot2
-  r |= ar(u + 6, u + 6, 4, 5, 0, comm, s);   // kept, blocks, stream_bytes, field_bytes
-  r |= ar(u + 10, u + 10, 1, 5, 0, comm, s); // status lanes (sum)
-  r |= ge();
+  double* d = reinterpret_cast<double*>(d_stats);
+  stats_pack_kernel<<<1, 256, 0, s>>>(u, n, 0);
+  CUDA_TRY(cudaGetLastError());
+  int r = N.gs();
+  r |= N.ar(d, d, 4 * (size_t)n, 8, 0, comm, s);                    // energies (sum)
+  r |= N.ar(d + 4 * n, d + 4 * n, 2 * (size_t)n, 8, 2, comm, s);    // Linf terms (max)
+  r |= N.ar(u + 6 * n, u + 6 * n, 5 * (size_t)n, 5, 0, comm, s);    // counts, bytes, status lanes (sum)
+  r |= N.ge();
   if (r) return fail(ISF_E_TASK_FAILED, "ncclAllReduce failed (%d)", r);
-  status_lanes_kernel<<<1, 1, 0, s>>>(u + 10, 1);
+  stats_pack_kernel<<<1, 256, 0, s>>>(u, n, 1);
   CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+int isf_lossy_allreduce(isf_lossy_stats* d_stats, void* comm, void* cuda_stream) {
+  return isf_lossy_allreduce_n(d_stats, 1, comm, cuda_stream);
 }
 
 }  // extern "C"

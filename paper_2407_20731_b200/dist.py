@@ -72,3 +72,27 @@ def global_report(stats: torch.Tensor) -> GlobalReport:
     est = 0.0 if f[F_TOT2] == 0 else math.sqrt(f[F_DISC2] / f[F_TOT2])
     cr = (float(i[I_FIELD]) - float(i[I_STREAM])) / float(i[I_FIELD]) if i[I_FIELD] else 0.0
     return GlobalReport(rl2, rli, est, cr, i[I_KEPT], i[I_STREAM], i[I_FIELD])
+
+
+def nccl_comm_ptr(group=None, device=None) -> int:
+    """The ncclComm_t of torch.distributed's NCCL backend for `device` (0 if the group
+    is not NCCL): handed to the C ABI's isf_lossy_allreduce_n."""
+    pg = group if group is not None else dist.distributed_c10d._get_default_group()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    try:
+        be = pg._get_backend(dev)
+        return int(be._comm_ptr())
+    except Exception:
+        return 0
+
+
+def allreduce_stats_nccl(stats: torch.Tensor, comm: int, cuda_stream) -> None:
+    """In-place global reduction of n consecutive isf_lossy_stats records (a [n, 12]
+    float64 CUDA tensor) through the C ABI (isf_lossy_allreduce_n: one NCCL group of
+    three all-reduces), asynchronous on `cuda_stream`."""
+    import ctypes
+    from . import _native
+    from .lossy import _check
+    n = stats.numel() // 12
+    _check(_native.lib().isf_lossy_allreduce_n(ctypes.c_void_p(stats.data_ptr()), n, ctypes.c_void_p(comm),
+                                               ctypes.c_void_p(cuda_stream.cuda_stream)))
