@@ -20,6 +20,7 @@
 #include <cstring>
 #include <span>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -118,10 +119,11 @@ inline isf_lossy_plan* plan_for(std::uint32_t P, std::uint32_t comps) {
     int dev = 0;
     cudaGetDevice(&dev);
     struct Key { std::uint32_t P, c; int d; };
-    thread_local std::vector<std::pair<Key, Plan*>> plans;
+    // owned by the thread: destroyed (isf_lossy_plan_destroy) when the thread exits
+    thread_local std::vector<std::pair<Key, std::unique_ptr<Plan>>> plans;
     for (auto& kv : plans)
         if (kv.first.P == P && kv.first.c == comps && kv.first.d == dev) return kv.second->get();
-    plans.push_back({Key{P, comps, dev}, new Plan(P, comps, dev)});
+    plans.emplace_back(Key{P, comps, dev}, std::make_unique<Plan>(P, comps, dev));
     return plans.back().second->get();
 }
 }  // namespace detail
@@ -137,12 +139,14 @@ inline CompressedBlock lossy_compress(const Field& f, const LossyConfig& cfg) {
     b.components = f.components;
     b.n_elements = f.element_count();
     const std::uint64_t cap = isf_lossy_stream_capacity(f.points_per_element_axis, f.components, b.n_elements);
-    b.stream.resize(cap);
+    // worst-case scratch without value-initialisation (F + masks + counts), then a
+    // right-sized owned copy of the C bytes actually produced
+    std::unique_ptr<std::byte[]> scratch(new std::byte[cap]);
     std::uint64_t n = 0;
     isf_lossy_stats st{};
     detail::check(isf_lossy_compress_host(plan, f.values.data(), b.n_elements, cfg.max_error,
-                                          static_cast<int>(cfg.error_norm), b.stream.data(), cap, &n, &st));
-    b.stream.resize(n);
+                                          static_cast<int>(cfg.error_norm), scratch.get(), cap, &n, &st));
+    b.stream.assign(scratch.get(), scratch.get() + n);
     b.kept_total = st.kept;
     b.report = CompressionReport::from_sizes(st.field_bytes, n);
     return b;
@@ -154,6 +158,8 @@ inline Field lossy_decompress(const CompressedBlock& b, const Field& shape, Erro
     if (b.points_per_element_axis != shape.points_per_element_axis || b.components != shape.components ||
         b.n_elements != shape.element_count())
         throw Error(ErrorCode::ShapeMismatch, "compressed block does not match the requested field shape");
+    if (original && original->values.size() != shape.value_count())
+        throw Error(ErrorCode::ShapeMismatch, "original field does not match the requested field shape");
     auto* plan = detail::plan_for(b.points_per_element_axis, b.components);
     std::vector<double> out(shape.value_count());
     isf_lossy_stats st{};

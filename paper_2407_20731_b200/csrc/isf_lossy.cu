@@ -151,18 +151,21 @@ struct isf_lossy_plan {
 
 namespace {
 
-// ntiles: look-back descriptors; nparts: partial slots; noff: block-offset entries
-int ensure(isf_lossy_plan* p, size_t ntiles, size_t nparts, size_t noff) {
+// ntiles: look-back descriptors; nparts: partial slots; noff: block-offset entries.
+// Growth: cudaFree synchronises the device (no kernel of an earlier call still uses the
+// old buffers) and the zeroing is ordered on the caller's stream s, before the kernels
+// that accumulate into / look back on the new buffers.
+int ensure(isf_lossy_plan* p, size_t ntiles, size_t nparts, size_t noff, cudaStream_t s) {
   if (ntiles > p->status_cap) {
     if (p->status) cudaFree(p->status);
     if (p->csum) cudaFree(p->csum);
     p->csum = nullptr;
     size_t cap = std::max<size_t>(ntiles, 1024);
     CUDA_TRY(cudaMalloc(&p->status, cap * sizeof(uint64_t)));
-    CUDA_TRY(cudaMemset(p->status, 0, cap * sizeof(uint64_t)));
+    CUDA_TRY(cudaMemsetAsync(p->status, 0, cap * sizeof(uint64_t), s));
     p->csum_hw = 0;
     CUDA_TRY(cudaMalloc(&p->csum, 2 * cap * sizeof(uint64_t)));
-    CUDA_TRY(cudaMemset(p->csum, 0, 2 * cap * sizeof(uint64_t)));
+    CUDA_TRY(cudaMemsetAsync(p->csum, 0, 2 * cap * sizeof(uint64_t), s));
     p->status_cap = cap;
   }
   if (noff > p->toff_cap) {
@@ -210,14 +213,36 @@ cudaError_t launch_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
+// The single-pass lx = 8 schedule spins on the per-round aggregates of every CTA, so all
+// CTAs must be co-resident: a cooperative launch guarantees it (or fails, e.g. when
+// other work or MPS limits the SMs, and the caller falls back to the two-pass schedule).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_coop_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 template <int LX>
 int launch_compress_generic(isf_lossy_plan* p, CompressArgs a, cudaStream_t s) {
   const size_t sm = GenSmem<LX>::bytes;
-  static bool attr_set[64] = {};
-  if (!attr_set[p->device]) {
-    CUDA_TRY(cudaFuncSetAttribute(compress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr_set[p->device] = true;
-  }
+  static std::once_flag attr_once[64];
+  cudaError_t ae = cudaSuccess;
+  std::call_once(attr_once[p->device & 63], [&] {
+    ae = cudaFuncSetAttribute(compress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  });
+  CUDA_TRY(ae);
   int occ = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress_generic<LX>, kGenCThreads, sm));
   occ = std::max(occ, 1);
@@ -231,11 +256,12 @@ int launch_compress_generic(isf_lossy_plan* p, CompressArgs a, cudaStream_t s) {
 template <int LX>
 int launch_decompress_generic(isf_lossy_plan* p, DecompressArgs a, cudaStream_t s, uint32_t* grid_out) {
   const size_t sm = GenDSmem<LX>::bytes;
-  static bool attr_set[64] = {};
-  if (!attr_set[p->device]) {
-    CUDA_TRY(cudaFuncSetAttribute(decompress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr_set[p->device] = true;
-  }
+  static std::once_flag attr_once[64];
+  cudaError_t ae = cudaSuccess;
+  std::call_once(attr_once[p->device & 63], [&] {
+    ae = cudaFuncSetAttribute(decompress_generic<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  });
+  CUDA_TRY(ae);
   int occ = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress_generic<LX>, gen_dthreads<LX>(), sm));
   occ = std::max(occ, 1);
@@ -350,10 +376,10 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
                                   d8_smem<false>()));
     CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   d8_smem<true>()));
+    CUDA_TRY(cudaFuncSetAttribute(compress8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel<true>, kC8Warps * 32, kC8Smem));
     p->grid8c = p->sms * std::max(occ, 1);
-    CUDA_TRY(cudaFuncSetAttribute(compress8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
     {
       const char* e = getenv("ISF_C8_KERNEL");  // dev override of the default schedule
       if (e && strcmp(e, "singlepass") == 0) p->use_sp = true;
@@ -365,7 +391,10 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
                                                            d8_smem<true>()));
     p->grid8de = p->sms * std::max(occ, 1);
   }
-  CUDA_TRY(ensure(p, 1 << 16, 1 << 14, 1 << 16) == 0 ? cudaSuccess : cudaErrorMemoryAllocation);
+  CUDA_TRY(ensure(p, 1 << 16, 1 << 14, 1 << 16, 0) == 0 ? cudaSuccess : cudaErrorMemoryAllocation);
+  // the zeroing above ran on the legacy stream: complete it before any caller stream
+  // (possibly non-blocking) can use the plan
+  CUDA_TRY(cudaDeviceSynchronize());
   *out = p;
   return 0;
 }
@@ -437,7 +466,7 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
   const uint32_t ntiles = (uint32_t)B;  // generic: one tile per block; fast: one warp per block
   const uint32_t nchunks8 = (ntiles + kOffChunk - 1) / kOffChunk;
   const size_t nparts = fast ? (size_t)p->grid8c * kC8Warps : (size_t)ntiles;
-  if (int rc = ensure(p, fast ? nchunks8 : ntiles, nparts, B + 1)) return rc;
+  if (int rc = ensure(p, fast ? nchunks8 : ntiles, nparts, B + 1, s)) return rc;
   CompressArgs a;
   a.field = d_field;
   a.nblocks = B;
@@ -472,14 +501,18 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
         p->rstat = nullptr;
         p->rstat_cap = 0;
         CUDA_TRY(cudaMalloc(&p->rstat, need * sizeof(uint64_t)));
-        CUDA_TRY(cudaMemset(p->rstat, 0, need * sizeof(uint64_t)));
+        CUDA_TRY(cudaMemsetAsync(p->rstat, 0, need * sizeof(uint64_t), s));
         p->rstat_cap = need;
       }
       Sp8Args sp{p->rstat, a.ws.epoch, nrounds, reinterpret_cast<double*>(a.stream + a.val_off), cap_vals,
                  p->toff + B, f};
-      CUDA_TRY(launch_pdl(compress8_kernel<true>, grid, kC8Warps * 32, kC8Smem, s, a, sp));
-      p->last_launches = 1;
-      return 0;
+      const cudaError_t le = launch_coop_pdl(compress8_kernel<true>, grid, kC8Warps * 32, kC8Smem, s, a, sp);
+      if (le == cudaSuccess) {
+        p->last_launches = 1;
+        return 0;
+      }
+      if (le != cudaErrorCooperativeLaunchTooLarge) CUDA_TRY(le);
+      (void)cudaGetLastError();  // not co-resident now: two-pass schedule below
     }
     // two-pass: per-block value slots, packed by compact8_kernel
     const size_t slot_bytes = (size_t)B * 512 * sizeof(double);
@@ -589,7 +622,7 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
   const uint32_t nchunks8 = (ntiles + kOffChunk - 1) / kOffChunk;
   const size_t nparts = fast ? std::max<size_t>((size_t)p->grid8d * kD8Warps, (size_t)p->grid8de * kD8WarpsErr)
                              : (size_t)p->sms * 16;
-  if (int rc = ensure(p, std::max<uint32_t>(nchunks8, 1), nparts, B + 1)) return rc;
+  if (int rc = ensure(p, std::max<uint32_t>(nchunks8, 1), nparts, B + 1, s)) return rc;
   DecompressArgs a;
   a.stream = (const uint8_t*)d_stream;
   a.stream_bytes = stream_bytes;

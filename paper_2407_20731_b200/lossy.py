@@ -399,7 +399,9 @@ def lossy_compress(field: Field, cfg: LossyConfig, *, plan: LossyPlan | None = N
     rep = CompressionReport.from_sizes(st.field_bytes, nb.value)
     est = {"disc2": st.disc2, "tot2": st.tot2,
            "rel_l2_estimate": math.sqrt(st.disc2 / st.tot2) if st.tot2 > 0 else 0.0}
-    return CompressedBlock(buf[: nb.value], n_el, field.points_per_element_axis, field.components,
+    # right-sized result: the worst-case capacity buffer (F + masks + counts) goes back
+    # to the allocator instead of being kept alive by a view of its first C bytes
+    return CompressedBlock(buf[: nb.value].clone(), n_el, field.points_per_element_axis, field.components,
                            int(st.kept), rep, estimate=est)
 
 
@@ -456,8 +458,13 @@ def _decompress(block: CompressedBlock, shape, original: torch.Tensor | None):
     cs = torch.cuda.current_stream(dev)
     orig = None
     if original is not None:
+        if original.dtype != torch.float64 or original.numel() != n:
+            raise IsfError(ErrorCode.ShapeMismatch,
+                           f"original: {original.numel()} {original.dtype} values, the block decodes to {n} float64")
         orig = original if original.is_cuda else original.cuda()
         orig = orig.contiguous()
+        if orig.data_ptr() % 16:
+            orig = orig.clone()
     _check(plan._lib.isf_lossy_decompress(plan.handle, ctypes.c_void_p(s.data_ptr()), s.numel(),
                                           block.n_elements, ctypes.c_void_p(out.data_ptr()),
                                           ctypes.c_void_p(orig.data_ptr()) if orig is not None else None,
