@@ -1302,9 +1302,12 @@ __global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decom
       // Low cube (the common smooth case): every kept coefficient has kx, ky, kz < 4.
       // The inverse then runs on 16 x-lines, 32 y-lines and 64 z-lines instead of 64
       // each, one line per lane for x and y (the same pinned chains as inv2_low8),
-      // with two small padded shared-memory re-layouts (stride 9 doubles).
-      double* fx = reinterpret_cast<double*>(sp);  // [16 x-lines (kz, ky)][9]
-      double* fy = fx + 16 * 9;                    // [32 y-lines (kz, x)][9]
+      // with two small padded shared-memory re-layouts: line m at 10 m + (m >> 3), which
+      // keeps every half-warp's 16 doubles in distinct bank pairs for the x-line stores,
+      // the y-line loads and stores and the z-line loads (a stride of 9 was 2-way
+      // conflicted on the y-line loads and the z-line loads).
+      double* fx = reinterpret_cast<double*>(sp);  // [16 x-lines (kz, ky)]: 10 L + (L >> 3) + x
+      double* fy = fx + 160;                       // [32 y-lines (kz, x)]:  10 M + (M >> 3) + y
       {
         const int L = lane & 15, lky = L & 3;
         const int ml = 4 * (L >> 2) + (lky >> 1);  // mask lane of the line (kz, ky)
@@ -1321,7 +1324,7 @@ __global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decom
         __syncwarp();            // the values region is read: reuse the stage
         if (lane < 16) {
 #pragma unroll
-          for (int x = 0; x < 8; ++x) fx[L * 9 + x] = a8[x];
+          for (int x = 0; x < 8; ++x) fx[L * 10 + (L >> 3) + x] = a8[x];
         }
       }
       __syncwarp();
@@ -1329,16 +1332,16 @@ __global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decom
         const int ykz = lane >> 3, yx = lane & 7;
         double b8[8];
 #pragma unroll
-        for (int ky = 0; ky < 4; ++ky) b8[ky] = fx[(4 * ykz + ky) * 9 + yx];
+        for (int ky = 0; ky < 4; ++ky) b8[ky] = fx[(4 * ykz + ky) * 10 + (ykz >> 1) + yx];
         inv1_low8<1, 0, 1>(b8);  // inverse y sweep
 #pragma unroll
-        for (int yy = 0; yy < 8; ++yy) fy[(8 * ykz + yx) * 9 + yy] = b8[yy];
+        for (int yy = 0; yy < 8; ++yy) fy[(8 * ykz + yx) * 10 + ykz + yy] = b8[yy];
       }
       __syncwarp();
 #pragma unroll
       for (int z = 0; z < 4; ++z) {
-        v[2 * z] = fy[(8 * z + 2 * q) * 9 + y];
-        v[2 * z + 1] = fy[(8 * z + 2 * q + 1) * 9 + y];
+        v[2 * z] = fy[(8 * z + 2 * q) * 10 + z + y];
+        v[2 * z + 1] = fy[(8 * z + 2 * q + 1) * 10 + z + y];
       }
     } else {
     const double* sv = sv0 + inoff;
