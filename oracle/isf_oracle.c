@@ -142,50 +142,8 @@ static inline void inv_line(int n, const double* B, const double* a, int sa, dou
     for (int i = 0; i < n; ++i) u[i * su] = out[i];
 }
 
-/* lx = 8 forward: the sm_100a kernel runs the y and z sweeps on the
- * FP64 tensor cores (mma.m8n8k4.f64, two k-steps chained through the accumulator:
- * measured on the B200 to be a chain of fused multiply-adds in k order,
- * tools/probe/dmma_probe.cu).  Its k-step s feeds input index 2q + s from lane
- * quad position q, so every output is the fma chain over the inputs in the order
- * 0, 2, 4, 6, 1, 3, 5, 7 starting from +0; the x sweep stays the even/odd line
- * transform. */
-static const int kDmmaOrder8[8] = {0, 2, 4, 6, 1, 3, 5, 7};
-static inline void dmma_line8(const double* M /* [out][in], row stride 8 */, const double* u, int su, double* a,
-                              int sa) {
-    for (int k = 0; k < 8; ++k) {
-        double acc = 0.0;
-        for (int t = 0; t < 8; ++t) acc = fma(M[k * 8 + kDmmaOrder8[t]], u[kDmmaOrder8[t] * su], acc);
-        a[k * sa] = acc;
-    }
-}
-
-static void fwd_block8(const double* F, const double* u, double* a) {
-    double t[8];
-    memcpy(a, u, sizeof(double) * 512);
-    for (int z = 0; z < 8; ++z) /* y sweep */
-        for (int x = 0; x < 8; ++x) {
-            dmma_line8(F, a + z * 64 + x, 8, t, 1);
-            for (int k = 0; k < 8; ++k) a[z * 64 + k * 8 + x] = t[k];
-        }
-    for (int y = 0; y < 8; ++y) /* z sweep */
-        for (int x = 0; x < 8; ++x) {
-            dmma_line8(F, a + y * 8 + x, 64, t, 1);
-            for (int k = 0; k < 8; ++k) a[k * 64 + y * 8 + x] = t[k];
-        }
-    for (int z = 0; z < 8; ++z) /* x sweep (even/odd) */
-        for (int y = 0; y < 8; ++y) {
-            fwd_line(8, F, a + z * 64 + y * 8, 1, t, 1);
-            for (int k = 0; k < 8; ++k) a[z * 64 + y * 8 + k] = t[k];
-        }
-}
-
-/* forward: z sweep, then y, then x (in place on a scratch copy); lx = 8: y, z on the
- * tensor-core chain, then x (fwd_block8) */
+/* forward: z sweep, then y, then x (in place on a scratch copy) */
 void iso_fwd_block(int lx, const double* F, const double* u, double* a) {
-    if (lx == 8) {
-        fwd_block8(F, u, a);
-        return;
-    }
     const int n = lx, n2 = lx * lx, n3 = n2 * lx;
     double t[ISO_MAX_LX];
     memcpy(a, u, sizeof(double) * (size_t)n3);

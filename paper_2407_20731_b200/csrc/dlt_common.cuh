@@ -9,7 +9,6 @@
 #pragma once
 #include <cstdint>
 #include <utility>
-#include <cuda.h>  // CUtensorMap (type only; encoded through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 namespace isf {
@@ -104,26 +103,6 @@ __device__ __forceinline__ void inv_line(double (&v)[N]) {
   }
 #pragma unroll
   for (int i = 0; i < LX; ++i) v[O + i * S] = out[i];
-}
-
-// lx = 8 y / z sweeps of the pinned order: the FP64 tensor-core chain --
-// every output is the fma chain over the inputs 0, 2, 4, 6, 1, 3, 5, 7 from +0 (two
-// m8n8k4 k-steps, input 2q + s at k-step s).  Scalar form for the generic kernels.
-template <int T = -1>
-__device__ __forceinline__ void dmma_line8_ptr(double* p, int stride) {
-  double v[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = p[i * stride];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    double acc = 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int i = (t < 4) ? 2 * t : 2 * (t - 4) + 1;
-      acc = __fma_rn(Fm<8, T>(k, i), v[i], acc);
-    }
-    p[k * stride] = acc;
-  }
 }
 
 // Line transform on a pointer with runtime stride (generic kernels; same order).

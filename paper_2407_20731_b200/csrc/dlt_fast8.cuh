@@ -544,15 +544,15 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
 }
 
 // --------------------------- compress ---------------------------------------
-// stage: the block's 4 KiB as loaded by the TMA tensor engine with the 128-byte swizzle
-// (viewed as 32 rows of 128 B, 16-B chunk c of row R at chunk c ^ (R % 8)), so the
-// lane loads of the DMMA layout below are bank-conflict free; 1024-B aligned.
-constexpr int kC8Stage = 4096;
+// stage: the block's 4 KiB as loaded by the TMA engine, re-used in place for the z -> y
+// re-layout with a plane stride of 33 16-B chunks (528 B; conflict free both ways)
+constexpr int kC8Stage = 33 * 8 * 16;
+// stages | selection scratch (radix: 3 x 64 u32; binned: 32 u64 candidates, then
+// 3 x 256 u32 bins at byte 256) | mbarriers
 constexpr int kC8Scratch = 32 * 8 + 3 * kSelBins * 4;
 static_assert(kC8Scratch >= 768, "radix_select16 needs 3 x 64 u32");
-// dynamic shared memory: [1024-B alignment slack | stages of all warps | per-warp scratch + mbarriers]
-constexpr int kC8WarpBytes = kC8Scratch + 128;
-constexpr int kC8Smem = 1024 + kC8Warps * kC8Stages * kC8Stage + kC8Warps * kC8WarpBytes;
+constexpr int kC8WarpBytes = kC8Stages * kC8Stage + kC8Scratch + 128;
+constexpr int kC8Smem = kC8Warps * kC8WarpBytes;
 // TMEM columns per warp: [0, 32) y->x re-layout buffer, then the parked coefficients
 // (one 32-column slot; three for the single-pass kernel, whose value writes trail the
 // selection by two rounds); the four warps of a lane quadrant (warp % 4) sit side by side.
@@ -580,39 +580,15 @@ struct Sp8Args {
   FinalizeArgs fin;
 };
 
-// FP64 tensor-core step of the lx = 8 sweeps: D = A B + C on an m8n8k4 tile (a chain of
-// fused multiply-adds in k order per output, measured: tools/probe/dmma_probe.cu)
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b, double c0, double c1) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
-               : "=d"(d0), "=d"(d1) : "d"(a), "d"(b), "d"(c0), "d"(c1));
-}
-// One lx = 8 sweep on the tensor cores over 8 tiles: lane (r = l/4, q = l%4) holds
-// v[8e + t] = X[row = 2q + e][col = r] of tile t; out[m = r][n = 2q + e] =
-// sum_i M[m][i] X[i][n] in the pinned order i = 0, 2, 4, 6, 1, 3, 5, 7 (k-step s takes
-// i = 2q + s), with fa_s = M[r][2q + s].  In place: v[8e + t] = out[r][2q + e] of tile t.
-__device__ __forceinline__ void dmma_sweep8(double (&v)[16], double fa0, double fa1) {
-#pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    double d0, d1;
-    dmma884(d0, d1, fa0, v[t], 0.0, 0.0);
-    dmma884(d0, d1, fa1, v[8 + t], d0, d1);
-    v[t] = d0;
-    v[8 + t] = d1;
-  }
-}
-
 template <bool SP>
-__global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A, Sp8Args S,
-                                                                  const __grid_constant__ CUtensorMap tmap) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+__global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A, Sp8Args S) {
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t s_tmem;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // stages 1024-B aligned (128-byte swizzle atoms)
-  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char* sbase = smem + warp * kC8Stages * kC8Stage;
-  unsigned char* wbase = smem + kC8Warps * kC8Stages * kC8Stage + warp * kC8WarpBytes;
-  unsigned long long* hist = reinterpret_cast<unsigned long long*>(wbase);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kC8Scratch);
+  unsigned char* wbase = smem + warp * kC8WarpBytes;
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(wbase + kC8Stages * kC8Stage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wbase + kC8Stages * kC8Stage + kC8Scratch);
+  const int yoff = (lane & 7) * 33 + (lane >> 3);  // y-line role (plane kz = l%8, x pair q = l/8)
   uint32_t* counts = reinterpret_cast<uint32_t*>(A.stream);
   uint16_t* masks16 = reinterpret_cast<uint16_t*>(A.stream + A.mask_off);
   const uint64_t W = (uint64_t)gridDim.x * kC8Warps;
@@ -640,26 +616,15 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   pdl_wait();  // the field / stream / workspace may come from the previous kernel
   pdl_launch_dependents();
   const uint32_t tx = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (SP ? 128u : 64u) * (uint32_t)(warp >> 2);
-  const uint32_t sbase_a = smem_u32(sbase), bars_a = smem_u32(bars);  // hoisted shared-window addresses
+  const uint32_t wbase_a = smem_u32(wbase), bars_a = smem_u32(bars);  // hoisted shared-window addresses
   const uint64_t pol_stream = l2_policy_evict_first();  // the field is read once
   const uint64_t pol_keep = l2_policy_evict_last();     // value slots: re-read by compact8_kernel
-  const uint64_t tmap_a = reinterpret_cast<uint64_t>(&tmap);
-  // the block = 32 rows of 128 B (rows 32 blk .. 32 blk + 31 of the 2-D tensor map)
   auto issue = [&](uint64_t blk, int st) {
     if (lane == 0 && blk < B) {
       mbar_arrive_tx_a(bars_a + 8u * st, 4096u);
-      asm volatile(
-          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-          " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(sbase_a + (uint32_t)(st * kC8Stage)),
-          "l"(tmap_a), "r"(0), "r"((int)(blk * 32)), "r"(bars_a + 8u * st), "l"(pol_stream)
-          : "memory");
+      bulk_g2s_hint_a(wbase_a + (uint32_t)(st * kC8Stage), A.field + blk * 512, 4096u, bars_a + 8u * st, pol_stream);
     }
   };
-  // DMMA operand layout: lane l = 4 r + q loads row (z = r, y = 2q + e) of
-  // the block, i.e. 128-B row l, chunk 4 e + c, swizzled to chunk (4 e + c) ^ (l % 8)
-  const uint32_t lrow = (uint32_t)lane * 128u | ((uint32_t)(lane & 7) << 4);
-  // A fragments of the tensor-core sweeps: F[r][2q + s] (y and z sweeps use the same)
-  const double fa0 = c_f8[0][2 * lane], fa1 = c_f8[0][2 * lane + 1];
 #pragma unroll
   for (int s = 0; s < kC8Stages; ++s) issue(gw + s * W, s);
   double tot_acc = 0.0, disc_acc = 0.0;
@@ -736,33 +701,70 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     const uint32_t tpark = tx + 32u + (SP ? 32u * (it % 3u) : 0u);
     uint32_t mask = 0, kept = 0;
     if (!SP || blk < B) {  // warp-uniform
-    const uint32_t stg = sbase_a + (uint32_t)(st * kC8Stage);
+    double2* sb = reinterpret_cast<double2*>(wbase + st * kC8Stage);
     mbar_wait_a(bars_a + 8u * st, (ph >> st) & 1u);
     ph ^= 1u << st;
     double v[16];
-    // lane (r = l/4, q = l%4): v[8 e + x] = u[z = r][y = 2q + e][x] (swizzled 16-B chunks)
+    // z-lines: lane = (y = l/4, q = l%4) holds x = 2q, 2q+1 of row y for all z
 #pragma unroll
-    for (int e = 0; e < 2; ++e)
+    for (int z = 0; z < 8; ++z) {
+      const double2 t = sb[z * 32 + lane];
+      v[2 * z] = t.x;
+      v[2 * z + 1] = t.y;
+    }
+    __syncwarp();
+#ifndef ISF_EXP_NOXFORM
+    lines8<0, 2, 0, 1, 2, false>(v);  // z sweep
+#endif
+    // z -> y re-layout through the stage (in place): 16-B chunk c of plane kz at
+    // kz * 33 + c (all reads of the stage are done)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        double lo, hi;
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(lo), "=d"(hi)
-                     : "r"(stg + (lrow ^ (uint32_t)((4 * e + c) << 4))));
-        v[8 * e + 2 * c] = lo;
-        v[8 * e + 2 * c + 1] = hi;
-      }
+    for (int kz = 0; kz < 8; ++kz) sb[kz * 33 + lane] = make_double2(v[2 * kz], v[2 * kz + 1]);
+    __syncwarp();
+    // y-lines: lane = (q = l/8, kz = l%8) holds x = 2q, 2q+1 for all y at plane kz
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      const double2 t = sb[yoff + 4 * y];
+      v[2 * y] = t.x;
+      v[2 * y + 1] = t.y;
+    }
     fence_proxy_async();
     __syncwarp();
     issue(blk + kC8Stages * W, st);  // the stage is free: refill it now
     st = (st + 1 == kC8Stages) ? 0 : st + 1;
 #ifndef ISF_EXP_NOXFORM
-    // y sweep (tile x, rows y -> ky, columns z): v[8 e + x] = [ky = r][z = 2q + e]
-    dmma_sweep8(v, fa0, fa1);
-    // z sweep (tile x, rows z -> kz, columns ky): v[8 e + x] = [kz = r][ky = 2q + e]
-    dmma_sweep8(v, fa0, fa1);
-    // x sweep on the lane's two x-lines: v[8 e + kx] = coefficient
-    // kx + 8 (2q + e) + 64 r = 16 lane + 8 e + kx
-    lines8<2, 1, 0, 8, 2, false>(v);
+    lines8<1, 2, 0, 1, 2, false>(v);  // y sweep: v[2 ky + x0]
+#endif
+    // y -> x re-layout through TMEM: store 32x32b with column pair
+    // c = (ky0, x0, ky2, ky1) [bits 3..0], re-read 16x256b at lanes 0 and 16.  Reader
+    // lane u gets (source lane bits 2..0, c bits 1..0) = (kz, ky2 ky1): the x-line
+    // role; its double (g, j, h) of instruction g, rep j, half h holds
+    // x2 = g, x1 = h, ky0 = j1, x0 = j0.
+    {
+      uint32_t r[32];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int ky = ((c >> 1) & 1) * 4 + (c & 1) * 2 + (c >> 3), x0 = (c >> 2) & 1;
+        r[2 * c] = (uint32_t)__double2loint(v[2 * ky + x0]);
+        r[2 * c + 1] = (uint32_t)__double2hiint(v[2 * ky + x0]);
+      }
+      tmem_st_32x32b_x32(tx, r);
+      tmem_wait_st();
+      uint32_t a0[16], a1[16];
+      tmem_ld_16x256b_x4(tx, a0);
+      tmem_ld_16x256b_x4(tx + (16u << 16), a1);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int dst = (j >> 1) * 8 + h * 2 + (j & 1);  // kyi * 8 + x, x = 4 g + 2 h + j0
+          v[dst] = __hiloint2double((int)a0[4 * j + 2 * h + 1], (int)a0[4 * j + 2 * h]);
+          v[dst + 4] = __hiloint2double((int)a1[4 * j + 2 * h + 1], (int)a1[4 * j + 2 * h]);
+        }
+    }
+#ifndef ISF_EXP_NOXFORM
+    lines8<2, 1, 0, 8, 2, false>(v);  // x sweep: v[r] = coefficient 16*lane + r
 #endif
     // park the coefficients in TMEM (one column pair per double: no register
     // marshalling); the registers are then free for the selection

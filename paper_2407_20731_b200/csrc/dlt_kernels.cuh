@@ -339,15 +339,9 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
       atomicMax(reinterpret_cast<unsigned long long*>(&misc[3]), (unsigned long long)um);
     }
     __syncthreads();
-    if constexpr (LX == 8) {  // lx = 8 pinned order: y, z on the tensor-core chain
-      for (int l = tid; l < N2; l += kGenCThreads) dmma_line8_ptr(u + (l / N) * N2 + (l % N), N);   // y
-      __syncthreads();
-      for (int l = tid; l < N2; l += kGenCThreads) dmma_line8_ptr(u + l, N2);                      // z
-    } else {
-      for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + l, N2);                       // z
-      __syncthreads();
-      for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + (l / N) * N2 + (l % N), N);  // y
-    }
+    for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + l, N2);                       // z
+    __syncthreads();
+    for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + (l / N) * N2 + (l % N), N);  // y
     __syncthreads();
     for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + l * N, 1);                     // x
     __syncthreads();

@@ -147,48 +147,9 @@ struct isf_lossy_plan {
   uint64_t* crc_n = nullptr;
   int grid8c = 0, grid8d = 0, grid8de = 0, gridg = 0;
   size_t smem_g = 0;
-  // 2-D tensor maps of the lx = 8 block view (32 rows of 128 B per block, 128-byte
-  // swizzle) for the TMA tensor loads / stores; re-encoded when the pointer or size changes
-  CUtensorMap tm_in{}, tm_out{};
-  const void* tm_in_ptr = nullptr;
-  const void* tm_out_ptr = nullptr;
-  uint64_t tm_in_blocks = 0, tm_out_blocks = 0;
 };
 
 namespace {
-
-// cuTensorMapEncodeTiled from the driver, resolved once through the runtime (no -lcuda)
-typedef CUresult (*encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-encode_tiled_fn encode_tiled() {
-  static encode_tiled_fn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = (encode_tiled_fn)f;
-  });
-  return fn;
-}
-
-// lx = 8 block view of a scalar field: rows of 16 doubles (128 B), 32 rows per block, box
-// = one block, 128-byte swizzle (conflict-free DMMA operand loads)
-int block_map8(CUtensorMap* m, const void* ptr, uint64_t nblocks) {
-  encode_tiled_fn enc = encode_tiled();
-  if (!enc) return fail(ISF_E_TASK_FAILED, "cuTensorMapEncodeTiled not available");
-  const cuuint64_t dims[2] = {16, (cuuint64_t)nblocks * 32};
-  const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {16, 32};
-  const cuuint32_t es[2] = {1, 1};
-  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(ISF_E_TASK_FAILED, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return 0;
-}
 
 // ntiles: look-back descriptors; nparts: partial slots; noff: block-offset entries.
 // Growth: cudaFree synchronises the device (no kernel of an earlier call still uses the
@@ -531,11 +492,6 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
     FinalizeArgs f{0, p->partials, parts, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
                    B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
     const uint64_t cap_vals = capacity > hdr ? (capacity - hdr) / 8 : 0;
-    if (p->tm_in_ptr != d_field || p->tm_in_blocks != B) {
-      if (int rc = block_map8(&p->tm_in, d_field, B)) return rc;
-      p->tm_in_ptr = d_field;
-      p->tm_in_blocks = B;
-    }
     if (p->use_sp) {
       const uint64_t W = (uint64_t)grid * kC8Warps;
       const uint32_t nrounds = (uint32_t)((B + W - 1) / W);
@@ -550,7 +506,7 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
       }
       Sp8Args sp{p->rstat, a.ws.epoch, nrounds, reinterpret_cast<double*>(a.stream + a.val_off), cap_vals,
                  p->toff + B, f};
-      const cudaError_t le = launch_coop_pdl(compress8_kernel<true>, grid, kC8Warps * 32, kC8Smem, s, a, sp, p->tm_in);
+      const cudaError_t le = launch_coop_pdl(compress8_kernel<true>, grid, kC8Warps * 32, kC8Smem, s, a, sp);
       if (le == cudaSuccess) {
         p->last_launches = 1;
         return 0;
@@ -568,7 +524,7 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
       p->vslot_cap = slot_bytes;
     }
     a.vslot = p->vslot;
-    CUDA_TRY(launch_pdl(compress8_kernel<false>, grid, kC8Warps * 32, kC8Smem, s, a, Sp8Args{}, p->tm_in));
+    CUDA_TRY(launch_pdl(compress8_kernel<false>, grid, kC8Warps * 32, kC8Smem, s, a, Sp8Args{}));
     CUDA_TRY(launch_pdl(compact8_kernel, nchunks8 + 1, kCompactThreads, 0, s, a.stream, B, a.mask_off,
                         (const uint64_t*)a.ws.csum, p->csum + (p->csum_par ^ 1) * p->status_cap,
                         (const double*)p->vslot, reinterpret_cast<double*>(a.stream + a.val_off), cap_vals,

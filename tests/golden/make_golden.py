@@ -148,34 +148,8 @@ def inv_line(B, a):
     return out
 
 
-DMMA_ORDER8 = (0, 2, 4, 6, 1, 3, 5, 7)
-
-
-def dmma_line8(M, u):
-    """lx = 8 y / z sweeps: the FP64 tensor-core chain (two m8n8k4 k-steps, input
-    index 2q + s at k-step s): fma over the inputs in DMMA_ORDER8, from +0."""
-    out = []
-    for k in range(8):
-        acc = 0.0
-        for i in DMMA_ORDER8:
-            acc = _fma(M[k][i], u[i], acc)
-        out.append(acc)
-    return out
-
-
 def fwd_block(F, u, n):
     a = np.array(u, dtype=float).reshape(n, n, n)  # [z][y][x]
-    if n == 8:  # y, z on the tensor-core chain, then x even/odd (DESIGN.md 3.3)
-        for z in range(n):
-            for x in range(n):
-                a[z, :, x] = dmma_line8(F, list(a[z, :, x]))
-        for y in range(n):
-            for x in range(n):
-                a[:, y, x] = dmma_line8(F, list(a[:, y, x]))
-        for z in range(n):
-            for y in range(n):
-                a[z, y, :] = fwd_line(F, list(a[z, y, :]))
-        return a.reshape(-1)
     for y in range(n):
         for x in range(n):
             a[:, y, x] = fwd_line(F, list(a[:, y, x]))
@@ -324,8 +298,8 @@ def main():
         out[f"{name}__meta"] = np.array([lx, eps])
         names.append(name)
     out["cases"] = np.array(names)
-    np.savez_compressed(os.path.join(HERE, "golden_v3.npz"), **out)
-    print("wrote", os.path.join(HERE, "golden_v3.npz"), names)
+    np.savez_compressed(os.path.join(HERE, "golden_v2.npz"), **out)
+    print("wrote", os.path.join(HERE, "golden_v2.npz"), names)
 
 
 if __name__ == "__main__":

@@ -6,7 +6,7 @@ import os
 import numpy as np
 import pytest
 
-GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_v3.npz")
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "golden_v2.npz")
 
 
 @pytest.fixture(scope="module")
@@ -48,7 +48,7 @@ def test_golden_generator_is_reproducible(tmp_path):
     spec.loader.exec_module(mg)
     mg.main()
     a = np.load(GOLDEN)
-    b = np.load(tmp_path / "golden_v3.npz")
+    b = np.load(tmp_path / "golden_v2.npz")
     assert sorted(a.files) == sorted(b.files)
     for k in a.files:
         assert np.array_equal(a[k], b[k]), k
