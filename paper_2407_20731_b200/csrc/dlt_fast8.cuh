@@ -427,6 +427,20 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   constexpr uint64_t C52 = 0x4330000000000000ull;
   double t[16];
   uint64_t t0 = 0, t1 = 0;
+  // f = 2^k folded into the scale constants: RD((a f)^2) = RD(a^2) 2^(2k) exactly while
+  // a^2 is normal; when it is subnormal, both sides stay below 2^-22 after scaling by
+  // at most 2^1000, so the floors agree (0)
+  const bool fold = 2 * k + h <= 1000;
+  if (fold) {
+    const double fA = pow2d(2 * k + h);
+#pragma unroll
+    for (int r = 0; r < 16; r += 2) {
+      t[r] = __dmul_rd(v[r], v[r]);
+      t[r + 1] = __dmul_rd(v[r + 1], v[r + 1]);
+      t0 += (uint64_t)__double_as_longlong(__fma_rd(t[r], fA, kTwo52));
+      t1 += (uint64_t)__double_as_longlong(__fma_rd(t[r + 1], fA, kTwo52));
+    }
+  } else {
 #pragma unroll
   for (int r = 0; r < 16; r += 2) {
     const double xa = __dmul_rn(v[r], f), xb = __dmul_rn(v[r + 1], f);
@@ -434,6 +448,7 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
     t[r + 1] = __dmul_rd(xb, xb);
     t0 += (uint64_t)__double_as_longlong(__fma_rd(t[r], sA, kTwo52));
     t1 += (uint64_t)__double_as_longlong(__fma_rd(t[r + 1], sA, kTwo52));
+  }
   }
   const uint64_t T = warp_sum_u58(t0 + t1 - 16 * C52);
   s.T = T;
@@ -443,8 +458,23 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
   s.eD = -2 * k0 - h - G;
   const double sB = pow2d(h + G);
   // scale B: t_r = 2^52 + floor(e_r 2^(h+G)) (>= 2^53: saturated, never discardable)
+  if (fold && 2 * k + h + G <= 1000) {
+    const double fB = pow2d(2 * k + h + G);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) t[r] = __fma_rd(t[r], fB, kTwo52);
+  } else if (fold) {  // (rare) the folded scale would exceed 2^1000: recompute from the parked copy
+    double c16[16];
+    tmem_wait_st();
+    tmem_load16(tpark, c16);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const double x = __dmul_rn(c16[r], f);
+      t[r] = __fma_rd(__dmul_rd(x, x), sB, kTwo52);
+    }
+  } else {
 #pragma unroll
   for (int r = 0; r < 16; ++r) t[r] = __fma_rd(t[r], sB, kTwo52);
+  }
   // kept-above-threshold set H: hi = lo + 1 > thr  <=>  lo >= thr  <=>  t >= 2^52 + thr
   const double tthr = __longlong_as_double((long long)(C52 + thr));  // thr < 2^52
   uint32_t mH = 0;
@@ -618,7 +648,6 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   const uint32_t tx = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (SP ? 128u : 64u) * (uint32_t)(warp >> 2);
   const uint32_t wbase_a = smem_u32(wbase), bars_a = smem_u32(bars);  // hoisted shared-window addresses
   const uint64_t pol_stream = l2_policy_evict_first();  // the field is read once
-  const uint64_t pol_keep = l2_policy_evict_last();     // value slots: re-read by compact8_kernel
   auto issue = [&](uint64_t blk, int st) {
     if (lane == 0 && blk < B) {
       mbar_arrive_tx_a(bars_a + 8u * st, 4096u);
@@ -782,11 +811,10 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       counts[blk] = kept;  // the 16-B pad is zeroed by compact8_kernel / the last CTA
       if (!SP && kept) atomicAdd(reinterpret_cast<unsigned long long*>(A.ws.csum + (blk >> 10)), (unsigned long long)kept);
     }
-    {  // mask words stay in L2 for compact8_kernel's gather (the field streams evict_first)
-      const uint16_t mw = (uint16_t)mask;
-      asm volatile("st.global.L2::cache_hint.b16 [%0], %1, %2;" ::"l"(masks16 + blk * 32 + lane), "h"(mw), "l"(pol_keep)
-                   : "memory");
-    }
+    // mask words and slots are plain stores: an evict_last hint here (for
+    // compact8_kernel's gather) left lines pinned in L2 that cost the next decompress
+    // 9 % and this kernel 2 % (profiles/r2_summary.md)
+    masks16[blk * 32 + lane] = (uint16_t)mask;
     // kept values from the parked copy into the block's slot at their natural index
     // (slot[j] = a_j for kept j): one TMEM load and sixteen predicated stores with
     // immediate offsets; compact8_kernel gathers them in index order via the mask
@@ -802,15 +830,13 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
 #pragma unroll
         for (int r = 0; r < 16; ++r)
           if ((mask >> r) & 1u)
-            asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(dst + r), "d"(c16[r]), "l"(pol_keep)
-                         : "memory");
+            dst[r] = c16[r];
       } else {
         double* dst = A.vslot + blk * 512 + lane;
 #pragma unroll
         for (int r = 0; r < 16; ++r)
           if ((mask >> r) & 1u)
-            asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(dst + 32 * r), "d"(c16[r]), "l"(pol_keep)
-                         : "memory");
+            dst[32 * r] = c16[r];
       }
     }
     if (!sel.nonfinite && sel.T) {
