@@ -16,6 +16,7 @@
 // include path and link libisf_lossy.so.  The transform is the
 // per-element Legendre/GLL DLT of north_star (SPEC.md:205 says DCT-II).
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <span>
@@ -208,7 +209,9 @@ inline Bytes lossy_compress_frame(const double* d_field, std::uint64_t n_element
         void* frame = nullptr;
         std::uint64_t cap = 0;
         isf_lossy_stats* stats = nullptr;
-        ~Bufs() { cudaFree(frame); cudaFree(stats); }
+        std::byte* pinned = nullptr;  // page-locked staging of the frame (full-speed D2H)
+        std::uint64_t pinned_cap = 0;
+        ~Bufs() { cudaFree(frame); cudaFree(stats); cudaFreeHost(pinned); }
     };
     thread_local Bufs b;
     const std::uint64_t cap = isf_lossy_stream_capacity(P, comps, n_elements) + ISF_FRAME_OVERHEAD;
@@ -228,23 +231,27 @@ inline Bytes lossy_compress_frame(const double* d_field, std::uint64_t n_element
         throw Error(ErrorCode::TaskFailed, "frame statistics copy failed");
     if (st.status & ISF_STATUS_NONFINITE) throw Error(ErrorCode::InvalidArgument, "Field: non-finite value");
     if (st.status) throw Error(ErrorCode::SerializationFailed, "frame assembly failed");
-    Bytes out(st.stream_bytes + ISF_FRAME_OVERHEAD);
-    if (cudaMemcpy(out.data(), b.frame, out.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    const std::uint64_t fbytes = st.stream_bytes + ISF_FRAME_OVERHEAD;
+    if (fbytes > b.pinned_cap) {  // grows (x1.5 headroom) with the frames seen, not to the capacity bound
+        cudaFreeHost(b.pinned);
+        b.pinned = nullptr;
+        b.pinned_cap = 0;
+        const std::uint64_t want = std::min<std::uint64_t>(b.cap, fbytes + fbytes / 2);
+        if (cudaMallocHost(reinterpret_cast<void**>(&b.pinned), want) != cudaSuccess)
+            throw Error(ErrorCode::TaskFailed, "cudaMallocHost frame staging");
+        b.pinned_cap = want;
+    }
+    if (cudaMemcpyAsync(b.pinned, b.frame, fbytes, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess)
         throw Error(ErrorCode::TaskFailed, "frame copy failed");
-    return out;
+    return Bytes(b.pinned, b.pinned + fbytes);  // the owned frame StageWriter::write_frame takes
 }
 
-/// Inverse of CompressedBlock::payload(): a block from a kind-1 payload (the
-/// stream is everything before the SPEC.md:282 codec trailer).
-inline CompressedBlock block_from_payload(std::span<const std::byte> payload, const FrameHeader& h,
-                                          std::uint64_t n_elements) {
+/// Length of the stream at the front of a kind-1 payload: its header plus 8 bytes
+/// per stored value (the counts say how many); the SPEC.md:282 codec trailer follows.
+inline std::size_t kind1_stream_bytes(std::span<const std::byte> payload, const FrameHeader& h,
+                                      std::uint64_t n_elements) {
     if (payload.size() < 10) throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its trailer");
-    CompressedBlock b;
-    b.elements_per_axis = h.elements_per_axis;
-    b.points_per_element_axis = h.points_per_element_axis;
-    b.components = h.components;
-    b.n_elements = n_elements;
-    // the stream length follows from its own counts: header + 8 * sum(counts)
     const std::uint64_t B = n_elements * h.components;
     const std::uint64_t hdr = isf_lossy_stream_header_bytes(h.points_per_element_axis, h.components, n_elements);
     if (payload.size() < hdr + 10) throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its header");
@@ -259,13 +266,29 @@ inline CompressedBlock block_from_payload(std::span<const std::byte> payload, co
     std::uint64_t coded = 0;
     std::memcpy(&coded, payload.data() + sb + 2, 8);
     if (sb + 10 + coded != payload.size()) throw Error(ErrorCode::LengthMismatch, "kind-1 payload length mismatch");
-    b.stream.assign(payload.begin(), payload.begin() + sb);
+    return sb;
+}
+
+/// Inverse of CompressedBlock::payload(): a block from a kind-1 payload (the
+/// stream is everything before the SPEC.md:282 codec trailer).  keep_stream = false
+/// leaves the stream out (metadata, codec trailer and report only).
+inline CompressedBlock block_from_payload(std::span<const std::byte> payload, const FrameHeader& h,
+                                          std::uint64_t n_elements, bool keep_stream = true) {
+    CompressedBlock b;
+    b.elements_per_axis = h.elements_per_axis;
+    b.points_per_element_axis = h.points_per_element_axis;
+    b.components = h.components;
+    b.n_elements = n_elements;
+    const std::size_t sb = kind1_stream_bytes(payload, h, n_elements);
+    std::uint64_t coded = 0;
+    std::memcpy(&coded, payload.data() + sb + 2, 8);
+    if (keep_stream) b.stream.assign(payload.begin(), payload.begin() + sb);
     b.lossless_codec = std::uint16_t(std::to_integer<std::uint8_t>(payload[sb])) |
                        std::uint16_t(std::uint16_t(std::to_integer<std::uint8_t>(payload[sb + 1])) << 8);
     b.coded_bytes.assign(payload.begin() + sb + 10, payload.begin() + sb + 10 + coded);
     b.report = CompressionReport::from_sizes(n_elements * h.points_per_element_axis * h.points_per_element_axis *
                                                  h.points_per_element_axis * h.components * 8,
-                                             b.stream.size());
+                                             sb);
     return b;
 }
 

@@ -53,7 +53,10 @@ class AsyncInSitu:
         if rc:
             raise IsfError(ErrorCode(rc - 1), _native.last_error())
 
-    def run(self, steps: int, every: int, compress: bool):
+    def run(self, steps: int, every: int, compress: bool, keep: list | None = None):
+        """`steps` solver steps, compressing every `every`-th state on the side stream.
+        keep: optional list that receives (step, [stream copy per field], stats copy) of
+        every compression, copied on the side stream (tests)."""
         ev = lambda: torch.cuda.Event(enable_timing=True)
         done = [None, None]
         t0, t1 = ev(), ev()
@@ -72,6 +75,9 @@ class AsyncInSitu:
                 for f in range(self.nf):
                     self.plan.compress_async(self.buf[target][f], self.n_el, self.eps, self.streams[f],
                                              self.stats[f], cuda_stream=self.side)
+                if keep is not None:
+                    with torch.cuda.stream(self.side):
+                        keep.append((n, [t.clone() for t in self.streams], self.stats.clone()))
                 d = torch.cuda.Event()
                 d.record(self.side)
                 done[target] = d
