@@ -36,7 +36,10 @@ namespace isf::tasks {
 enum class ErrorNorm { RelativeL2 = ISF_NORM_RELATIVE_L2, RelativeLInf = ISF_NORM_RELATIVE_LINF };
 
 struct LossyConfig {
-    double max_error = 1e-2;  // SPEC.md:205 paper value
+    // SPEC.md:205 paper value.  RelativeL2 bounds the GLL-quadrature (polynomial) L2
+    // norm of the error per block, not the plain point-sample norm (isf_lossy.h,
+    // DESIGN.md 3.8).
+    double max_error = 1e-2;
     ErrorNorm error_norm = ErrorNorm::RelativeL2;
 
     void validate() const {

@@ -57,7 +57,11 @@ enum {
 };
 
 /* LossyConfig.error_norm.  RelativeL2: exact Parseval energy rule
- * (DESIGN.md 3.4).  RelativeLInf: per block, sum over the discarded coefficients of
+ * (DESIGN.md 3.4), in the GLL-quadrature norm ||v||_w^2 = sum w_x w_y w_z v^2, i.e. the
+ * L2 norm of the element polynomials (the norm of NEKO's DLT; err2 / nrm2 below report
+ * it).  It bounds the plain point-sample relative L2 only up to sqrt(max w / min w) per
+ * element (about 40 at lx = 8; tests/test_oracle_norms.py), which is why SPEC.md's
+ * DCT-II wording (plain samples) and this transform differ.  RelativeLInf: per block, sum over the discarded coefficients of
  * |a_j| * max|basis_j| <= max_error * max|u| (a bound on the reconstruction's max
  * error; runs on the generic kernels). */
 enum { ISF_NORM_RELATIVE_L2 = 0, ISF_NORM_RELATIVE_LINF = 1 };

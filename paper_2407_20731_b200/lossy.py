@@ -74,7 +74,12 @@ class ErrorNorm(IntEnum):
 
 @dataclass(frozen=True)
 class LossyConfig:
-    """SPEC.md:204-207.  The transform is the per-element Legendre/GLL DLT (north_star)."""
+    """SPEC.md:204-207.  The transform is the per-element Legendre/GLL DLT (north_star).
+
+    RelativeL2 bounds the error in the GLL-quadrature norm (sum of w_x w_y w_z v^2: the
+    L2 norm of the element polynomials), which is the norm Parseval holds in for this
+    transform; the plain point-sample relative L2 is bounded only up to
+    sqrt(max w / min w) per element (tests/test_oracle_norms.py)."""
     max_error: float = 1e-2
     error_norm: ErrorNorm = ErrorNorm.RelativeL2
 
