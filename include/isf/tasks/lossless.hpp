@@ -169,10 +169,10 @@ inline Bytes lossless_decode(std::span<const std::byte> in, LosslessCodec codec,
 }
 
 /// Asynchronous suffix of the hybrid mode: drain `reader` (CRC-validated kind-1
-/// frames from the device prefix), lossless-code every block's stream with `codec`
-/// on `threads` host threads (straight from the frame, no copy) and hand the block
-/// (metadata, codec id, coded bytes; the stream too if keep_stream; its size is
-/// report.compressed_size) to `sink`.  Returns the number of frames consumed.  Runs
+/// frames from the device prefix), lossless-code every block's SPEC.md:282 payload
+/// body with `codec` on `threads` host threads (straight from the frame, no copy) and
+/// hand the block (metadata, codec id, coded bytes and coded_source_bytes; the mask
+/// stream too if keep_stream) to `sink`.  Returns the number of frames consumed.  Runs
 /// on the caller's (consumer) thread.
 inline std::uint64_t run_lossless_suffix(staging::StageReader& reader, std::uint64_t n_elements, LosslessCodec codec,
                                          int threads, const std::function<void(std::uint64_t, CompressedBlock&&)>& sink,
@@ -184,7 +184,9 @@ inline std::uint64_t run_lossless_suffix(staging::StageReader& reader, std::uint
             throw Error(ErrorCode::InvalidArgument, "hybrid suffix: frame is not a compressed block");
         const auto payload = fr->payload();
         CompressedBlock blk = block_from_payload(payload, h, n_elements, keep_stream);
-        LosslessResult r = lossless_encode(payload.first(blk.report.compressed_size), codec, threads);
+        const std::size_t body = kind1_body_bytes(payload, n_elements);
+        LosslessResult r = lossless_encode(payload.first(body), codec, threads);  // the SPEC.md:282 body
+        blk.coded_source_bytes = body;
         blk.lossless_codec = static_cast<std::uint16_t>(codec);
         blk.coded_bytes = std::move(r.coded);
         sink(h.step_index, std::move(blk));

@@ -66,9 +66,88 @@ struct ErrorReport {
     double rel_linf() const { return u_inf == 0.0 ? (err_inf == 0.0 ? 0.0 : 1.0 / 0.0) : err_inf / u_inf; }
 };
 
+namespace detail {
+/// SPEC.md:282 payload body (kept_count u32 per element | index u32 | value f64, index =
+/// component * P^3 + j ascending inside the element) from the mask stream; the host
+/// restatement of the device conversion (csrc/crc32.cuh spec_frame_kernel).
+inline Bytes spec_body_from_stream(std::span<const std::byte> stream, std::uint64_t n_el, std::uint32_t P,
+                                   std::uint32_t comps) {
+    const std::uint64_t P3 = std::uint64_t(P) * P * P, W = (P3 + 63) / 64, B = n_el * comps;
+    const std::uint64_t m0 = (4 * B + 15) & ~std::uint64_t(15), v0 = m0 + 8 * W * B;
+    if (stream.size() < v0) throw Error(ErrorCode::ShapeMismatch, "stream shorter than its header");
+    const std::uint64_t K = (stream.size() - v0) / 8;
+    Bytes out(4 * n_el + 12 * K);
+    std::uint64_t k = 0;
+    for (std::uint64_t e = 0; e < n_el; ++e) {
+        std::uint32_t ce = 0;
+        for (std::uint32_t c = 0; c < comps; ++c) {
+            const std::uint64_t b = e * comps + c;
+            std::uint32_t cnt;
+            std::memcpy(&cnt, stream.data() + 4 * b, 4);
+            ce += cnt;
+            for (std::uint64_t w = 0; w < W; ++w) {
+                std::uint64_t m;
+                std::memcpy(&m, stream.data() + m0 + 8 * (b * W + w), 8);
+                for (; m; m &= m - 1) {
+                    if (k >= K) throw Error(ErrorCode::ShapeMismatch, "stream masks exceed its values");
+                    const std::uint32_t idx = std::uint32_t(c * P3 + 64 * w + std::uint64_t(__builtin_ctzll(m)));
+                    std::memcpy(out.data() + 4 * n_el + 4 * k, &idx, 4);
+                    ++k;
+                }
+            }
+        }
+        std::memcpy(out.data() + 4 * e, &ce, 4);
+    }
+    if (k != K) throw Error(ErrorCode::ShapeMismatch, "stream masks and values disagree");
+    std::memcpy(out.data() + 4 * n_el + 4 * K, stream.data() + v0, 8 * K);
+    return out;
+}
+/// Inverse: the mask stream from a SPEC.md:282 payload body (ShapeMismatch when the
+/// indices are out of range or not ascending inside an element).
+inline Bytes stream_from_spec_body(std::span<const std::byte> body, std::uint64_t n_el, std::uint32_t P,
+                                   std::uint32_t comps) {
+    const std::uint64_t P3 = std::uint64_t(P) * P * P, W = (P3 + 63) / 64, B = n_el * comps;
+    if (body.size() < 4 * n_el) throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its counts");
+    std::uint64_t K = 0;
+    for (std::uint64_t e = 0; e < n_el; ++e) {
+        std::uint32_t c;
+        std::memcpy(&c, body.data() + 4 * e, 4);
+        K += c;
+    }
+    if (body.size() != 4 * n_el + 12 * K) throw Error(ErrorCode::LengthMismatch, "kind-1 payload body length");
+    const std::uint64_t m0 = (4 * B + 15) & ~std::uint64_t(15), v0 = m0 + 8 * W * B;
+    Bytes out(v0 + 8 * K, std::byte{0});
+    std::uint64_t k = 0;
+    for (std::uint64_t e = 0; e < n_el; ++e) {
+        std::uint32_t ce;
+        std::memcpy(&ce, body.data() + 4 * e, 4);
+        std::int64_t prev = -1;
+        for (std::uint32_t q = 0; q < ce; ++q, ++k) {
+            std::uint32_t idx;
+            std::memcpy(&idx, body.data() + 4 * n_el + 4 * k, 4);
+            if (idx >= comps * P3 || std::int64_t(idx) <= prev)
+                throw Error(ErrorCode::ShapeMismatch, "kind-1 payload: index out of range or not ascending");
+            prev = idx;
+            const std::uint64_t b = e * comps + idx / P3, j = idx % P3;
+            std::uint32_t cnt;
+            std::memcpy(&cnt, out.data() + 4 * b, 4);
+            ++cnt;
+            std::memcpy(out.data() + 4 * b, &cnt, 4);
+            std::uint64_t m;
+            std::memcpy(&m, out.data() + m0 + 8 * (b * W + j / 64), 8);
+            m |= std::uint64_t(1) << (j % 64);
+            std::memcpy(out.data() + m0 + 8 * (b * W + j / 64), &m, 8);
+        }
+    }
+    std::memcpy(out.data() + v0, body.data() + 4 * n_el + 4 * K, 8 * K);
+    return out;
+}
+}  // namespace detail
+
 /// SPEC.md:208-211.  `stream` is the device encoding of include/isf_lossy.h
 /// (counts | masks | values) copied to the host; codec 0 / empty coded bytes
-/// until a lossless stage runs on it.
+/// until a lossless stage runs.  The kind-1 payload it frames as
+/// is SPEC.md:282's (payload()).
 struct CompressedBlock {
     std::uint32_t elements_per_axis = 0;
     std::uint32_t points_per_element_axis = 0;
@@ -78,11 +157,13 @@ struct CompressedBlock {
     Bytes stream;
     std::uint16_t lossless_codec = 0;
     Bytes coded_bytes;
+    std::uint64_t coded_source_bytes = 0;  // bytes the lossless codec coded (the SPEC payload body)
     CompressionReport report;
 
-    /// kind-1 payload (SPEC.md:282 codec trailer appended to the stream)
+    /// SPEC.md:282 kind-1 payload: kept_count u32 per element | index u32 | value f64 |
+    /// codec id u16 | coded length u64 | coded bytes
     Bytes payload() const {
-        Bytes out(stream);
+        Bytes out = detail::spec_body_from_stream(stream, n_elements, points_per_element_axis, components);
         put_u16(out, lossless_codec);
         put_u64(out, coded_bytes.size());
         out.insert(out.end(), coded_bytes.begin(), coded_bytes.end());
@@ -185,20 +266,22 @@ inline void lossy_compress_device(const double* d_field, std::uint64_t n_element
                                            static_cast<int>(cfg.error_norm), d_stream, capacity, d_stats, stream));
 }
 
-/// Device-resident kind-1 frame: compresses straight into
-/// d_frame + 48 and writes header, codec trailer and CRC-32 on the device
-/// (isf_lossy_frame_async).  d_frame holds stream capacity + ISF_FRAME_OVERHEAD
-/// bytes; the frame is d_stats->stream_bytes + ISF_FRAME_OVERHEAD bytes long.
+/// Device-resident kind-1 frame: compresses into d_stream, then
+/// converts it on the device into the SPEC.md:282 payload and writes header, codec
+/// trailer and CRC-32 (isf_lossy_frame_async).  d_frame holds
+/// isf_lossy_frame_capacity bytes; the frame is ISF_FRAME_OVERHEAD + 4 n_elements +
+/// 12 d_stats->kept bytes long.
 inline void lossy_compress_frame_device(const double* d_field, std::uint64_t n_elements, std::uint32_t E_ax,
                                         std::uint32_t P, std::uint32_t comps, const LossyConfig& cfg,
-                                        void* d_frame, std::uint64_t frame_cap, isf_lossy_stats* d_stats,
-                                        std::uint64_t step_index, double sim_time, cudaStream_t stream) {
+                                        void* d_stream, std::uint64_t stream_cap, void* d_frame,
+                                        std::uint64_t frame_cap, isf_lossy_stats* d_stats, std::uint64_t step_index,
+                                        double sim_time, cudaStream_t stream) {
     cfg.validate();
     auto* plan = detail::plan_for(P, comps);
     detail::check(isf_lossy_compress_async(plan, d_field, n_elements, cfg.max_error,
-                                           static_cast<int>(cfg.error_norm), static_cast<char*>(d_frame) + 48,
-                                           frame_cap - 48, d_stats, stream));
-    detail::check(isf_lossy_frame_async(plan, d_frame, frame_cap, d_stats, E_ax, step_index, sim_time, stream));
+                                           static_cast<int>(cfg.error_norm), d_stream, stream_cap, d_stats, stream));
+    detail::check(isf_lossy_frame_async(plan, d_frame, frame_cap, d_stream, n_elements, d_stats, E_ax, step_index,
+                                        sim_time, stream));
 }
 
 /// Synchronous prefix of the hybrid mode (SPEC.md run_hybrid):
@@ -211,30 +294,39 @@ inline Bytes lossy_compress_frame(const double* d_field, std::uint64_t n_element
     struct Bufs {
         void* frame = nullptr;
         std::uint64_t cap = 0;
+        void* stream = nullptr;
+        std::uint64_t scap = 0;
         isf_lossy_stats* stats = nullptr;
         std::byte* pinned = nullptr;  // page-locked staging of the frame (full-speed D2H)
         std::uint64_t pinned_cap = 0;
-        ~Bufs() { cudaFree(frame); cudaFree(stats); cudaFreeHost(pinned); }
+        ~Bufs() { cudaFree(frame); cudaFree(stream); cudaFree(stats); cudaFreeHost(pinned); }
     };
     thread_local Bufs b;
-    const std::uint64_t cap = isf_lossy_stream_capacity(P, comps, n_elements) + ISF_FRAME_OVERHEAD;
+    const std::uint64_t cap = isf_lossy_frame_capacity(P, comps, n_elements);
+    const std::uint64_t scap = isf_lossy_stream_capacity(P, comps, n_elements);
     if (cap > b.cap) {
         cudaFree(b.frame);
         b.frame = nullptr;
         if (cudaMalloc(&b.frame, cap) != cudaSuccess) throw Error(ErrorCode::TaskFailed, "cudaMalloc frame");
         b.cap = cap;
     }
+    if (scap > b.scap) {
+        cudaFree(b.stream);
+        b.stream = nullptr;
+        if (cudaMalloc(&b.stream, scap) != cudaSuccess) throw Error(ErrorCode::TaskFailed, "cudaMalloc stream");
+        b.scap = scap;
+    }
     if (!b.stats && cudaMalloc(&b.stats, sizeof(isf_lossy_stats)) != cudaSuccess)
         throw Error(ErrorCode::TaskFailed, "cudaMalloc stats");
-    lossy_compress_frame_device(d_field, n_elements, E_ax, P, comps, cfg, b.frame, b.cap, b.stats, step_index,
-                                sim_time, stream);
+    lossy_compress_frame_device(d_field, n_elements, E_ax, P, comps, cfg, b.stream, b.scap, b.frame, b.cap, b.stats,
+                                step_index, sim_time, stream);
     isf_lossy_stats st{};
     if (cudaMemcpyAsync(&st, b.stats, sizeof st, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
         cudaStreamSynchronize(stream) != cudaSuccess)
         throw Error(ErrorCode::TaskFailed, "frame statistics copy failed");
     if (st.status & ISF_STATUS_NONFINITE) throw Error(ErrorCode::InvalidArgument, "Field: non-finite value");
     if (st.status) throw Error(ErrorCode::SerializationFailed, "frame assembly failed");
-    const std::uint64_t fbytes = st.stream_bytes + ISF_FRAME_OVERHEAD;
+    const std::uint64_t fbytes = ISF_FRAME_OVERHEAD + 4 * n_elements + 12 * st.kept;
     if (fbytes > b.pinned_cap) {  // grows (x1.5 headroom) with the frames seen, not to the capacity bound
         cudaFreeHost(b.pinned);
         b.pinned = nullptr;
@@ -250,31 +342,28 @@ inline Bytes lossy_compress_frame(const double* d_field, std::uint64_t n_element
     return Bytes(b.pinned, b.pinned + fbytes);  // the owned frame StageWriter::write_frame takes
 }
 
-/// Length of the stream at the front of a kind-1 payload: its header plus 8 bytes
-/// per stored value (the counts say how many); the SPEC.md:282 codec trailer follows.
-inline std::size_t kind1_stream_bytes(std::span<const std::byte> payload, const FrameHeader& h,
-                                      std::uint64_t n_elements) {
-    if (payload.size() < 10) throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its trailer");
-    const std::uint64_t B = n_elements * h.components;
-    const std::uint64_t hdr = isf_lossy_stream_header_bytes(h.points_per_element_axis, h.components, n_elements);
-    if (payload.size() < hdr + 10) throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its header");
-    std::uint64_t total = 0;
-    for (std::uint64_t i = 0; i < B; ++i) {
+/// Length of the SPEC.md:282 body (counts, indices, values) at the front of a kind-1
+/// payload; the codec trailer (codec id u16 | coded length u64 | coded) follows.
+inline std::size_t kind1_body_bytes(std::span<const std::byte> payload, std::uint64_t n_elements) {
+    if (payload.size() < 4 * n_elements + 10)
+        throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its counts + codec trailer");
+    std::uint64_t K = 0;
+    for (std::uint64_t e = 0; e < n_elements; ++e) {
         std::uint32_t c = 0;
-        std::memcpy(&c, payload.data() + 4 * i, 4);
-        total += c;
+        std::memcpy(&c, payload.data() + 4 * e, 4);
+        K += c;
     }
-    const std::size_t sb = hdr + 8 * total;
-    if (payload.size() < sb + 10) throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its stream");
+    const std::size_t body = 4 * n_elements + 12 * K;
+    if (payload.size() < body + 10) throw Error(ErrorCode::LengthMismatch, "kind-1 payload shorter than its arrays");
     std::uint64_t coded = 0;
-    std::memcpy(&coded, payload.data() + sb + 2, 8);
-    if (sb + 10 + coded != payload.size()) throw Error(ErrorCode::LengthMismatch, "kind-1 payload length mismatch");
-    return sb;
+    std::memcpy(&coded, payload.data() + body + 2, 8);
+    if (body + 10 + coded != payload.size()) throw Error(ErrorCode::LengthMismatch, "kind-1 payload length mismatch");
+    return body;
 }
 
-/// Inverse of CompressedBlock::payload(): a block from a kind-1 payload (the
-/// stream is everything before the SPEC.md:282 codec trailer).  keep_stream = false
-/// leaves the stream out (metadata, codec trailer and report only).
+/// Inverse of CompressedBlock::payload(): a block from a kind-1 payload (SPEC.md:282
+/// body converted back into the mask stream).  keep_stream = false leaves the stream
+/// out (metadata, codec trailer and report only).
 inline CompressedBlock block_from_payload(std::span<const std::byte> payload, const FrameHeader& h,
                                           std::uint64_t n_elements, bool keep_stream = true) {
     CompressedBlock b;
@@ -282,13 +371,20 @@ inline CompressedBlock block_from_payload(std::span<const std::byte> payload, co
     b.points_per_element_axis = h.points_per_element_axis;
     b.components = h.components;
     b.n_elements = n_elements;
-    const std::size_t sb = kind1_stream_bytes(payload, h, n_elements);
+    const std::size_t body = kind1_body_bytes(payload, n_elements);
     std::uint64_t coded = 0;
-    std::memcpy(&coded, payload.data() + sb + 2, 8);
-    if (keep_stream) b.stream.assign(payload.begin(), payload.begin() + sb);
-    b.lossless_codec = std::uint16_t(std::to_integer<std::uint8_t>(payload[sb])) |
-                       std::uint16_t(std::uint16_t(std::to_integer<std::uint8_t>(payload[sb + 1])) << 8);
-    b.coded_bytes.assign(payload.begin() + sb + 10, payload.begin() + sb + 10 + coded);
+    std::memcpy(&coded, payload.data() + body + 2, 8);
+    b.kept_total = (body - 4 * n_elements) / 12;
+    const std::uint64_t W = (std::uint64_t(h.points_per_element_axis) * h.points_per_element_axis *
+                                 h.points_per_element_axis + 63) / 64;
+    const std::uint64_t B = n_elements * h.components;
+    const std::uint64_t sb = ((4 * B + 15) & ~std::uint64_t(15)) + 8 * W * B + 8 * b.kept_total;
+    if (keep_stream)
+        b.stream = detail::stream_from_spec_body(payload.first(body), n_elements, h.points_per_element_axis,
+                                                 h.components);
+    b.lossless_codec = std::uint16_t(std::to_integer<std::uint8_t>(payload[body])) |
+                       std::uint16_t(std::uint16_t(std::to_integer<std::uint8_t>(payload[body + 1])) << 8);
+    b.coded_bytes.assign(payload.begin() + body + 10, payload.begin() + body + 10 + coded);
     b.report = CompressionReport::from_sizes(n_elements * h.points_per_element_axis * h.points_per_element_axis *
                                                  h.points_per_element_axis * h.components * 8,
                                              sb);

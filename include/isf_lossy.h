@@ -155,17 +155,24 @@ int isf_lossy_crc32(isf_lossy_plan* plan, const void* d_data, uint64_t n, uint32
                     void* cuda_stream);
 
 /* Kind-1 frame on the device (proj/include/isf/core/frame.hpp:3-11,
- * proj/src/core/frame.cpp:9-25 build_frame, SPEC.md:282 payload):
+ * proj/src/core/frame.cpp:9-25 build_frame) with SPEC.md:282's payload, converted on
+ * the device from the compressed stream d_stream (n_elements elements; the stats of
+ * that compress call in d_stats, read on the device):
  *   [0,48) header "ISF1" | 1 | kind 1 | step | sim_time | E | P | components | 0 | payload_len
- *   [48, 48+S) the stream, which the caller has compressed in place (d_stream = d_frame + 48)
- *   codec id u16 = 0 | coded length u64 = 0 (no lossless stage) | CRC-32 u32 of all preceding bytes
- * S is read from d_stats->stream_bytes (the stats of that compress call), so the call is
- * fully asynchronous; the frame is S + ISF_FRAME_OVERHEAD bytes.  d_frame is 16-byte
- * aligned; a frame_cap that is too small sets ISF_STATUS_OVERFLOW in d_stats->status. */
+ *   payload: kept_count u32[n_elements] | index u32[K] | value f64[K] |
+ *            codec id u16 = 0 | coded length u64 = 0 (no lossless stage yet)
+ *   CRC-32 u32 of all preceding bytes
+ * K = d_stats->kept; index = component * P^3 + j (j = kx + P (ky + P kz)), ascending
+ * inside each element, values in the same order.  The frame is
+ * ISF_FRAME_OVERHEAD + 4 n_elements + 12 K bytes (at most isf_lossy_frame_capacity);
+ * a frame_cap that is too small sets ISF_STATUS_OVERFLOW in d_stats->status.  d_frame
+ * and d_stream are 16-byte aligned and distinct; fully asynchronous. */
 #define ISF_FRAME_OVERHEAD 62
-int isf_lossy_frame_async(isf_lossy_plan* plan, void* d_frame, uint64_t frame_cap,
-                          const isf_lossy_stats* d_stats, uint32_t elements_per_axis,
+int isf_lossy_frame_async(isf_lossy_plan* plan, void* d_frame, uint64_t frame_cap, const void* d_stream,
+                          uint64_t n_elements, const isf_lossy_stats* d_stats, uint32_t elements_per_axis,
                           uint64_t step_index, double sim_time, void* cuda_stream);
+/* Worst-case kind-1 frame bytes (every coefficient kept). */
+uint64_t isf_lossy_frame_capacity(uint32_t points_per_element_axis, uint32_t components, uint64_t n_elements);
 
 /* Eq. 1: (original - compressed) / original in fp64. */
 double isf_lossy_compression_ratio(uint64_t original_size, uint64_t compressed_size);

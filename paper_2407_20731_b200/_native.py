@@ -21,9 +21,9 @@ EXPORTS = (
     "isf_lossy_decompress_host", "isf_lossy_allreduce", "isf_lossy_allreduce_n", "isf_lossy_compression_ratio",
     "isf_lossy_last_error", "isf_lossy_error_code_name", "isf_lossy_plan_operators",
     "isf_lossy_plan_last_launches", "isf_lossy_plan_set_compress_mode", "isf_lossy_generate_tgv", "isf_lossy_generate_spectral",
-    "isf_lossy_solver_standin", "isf_lossy_crc32", "isf_lossy_frame_async",
+    "isf_lossy_solver_standin", "isf_lossy_crc32", "isf_lossy_frame_async", "isf_lossy_frame_capacity",
 )
-FRAME_OVERHEAD = 62  # ISF_FRAME_OVERHEAD: 48-B header + codec trailer (10 B) + CRC (4 B)
+FRAME_OVERHEAD = 62  # ISF_FRAME_OVERHEAD: 48-B header + codec trailer (10 B) + CRC (4 B); + 4 n_el + 12 K payload
 
 
 class Stats(ctypes.Structure):
@@ -77,7 +77,8 @@ def lib() -> ctypes.CDLL:
         "isf_lossy_generate_spectral": ([P, P, u64, u64, u64, P, P], i32),
         "isf_lossy_solver_standin": ([P, P, P, u64, f64, P], i32),
         "isf_lossy_crc32": ([P, P, u64, P, P], i32),
-        "isf_lossy_frame_async": ([P, P, u64, P, u32, u64, f64, P], i32),
+        "isf_lossy_frame_async": ([P, P, u64, P, u64, P, u32, u64, f64, P], i32),
+        "isf_lossy_frame_capacity": ([u32, u32, u64], u64),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

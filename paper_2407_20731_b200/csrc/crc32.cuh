@@ -168,35 +168,84 @@ __global__ void __launch_bounds__(kFinalThreads) crc_final_kernel(const uint32_t
   }
 }
 
-// Kind-1 frame header + codec trailer (frame.hpp:3-11) around the stream
-// already at frame + 48; n_out = bytes covered by the CRC (header + payload).
-__global__ void frame_header_kernel(uint8_t* frame, uint64_t frame_cap, const uint64_t* stream_bytes_dev,
-                                    uint32_t E, uint32_t P, uint32_t comps, uint64_t step, double sim_time,
-                                    uint64_t* n_out, unsigned long long* flags) {
-  if (threadIdx.x != 0) return;
-  const uint64_t sb = *stream_bytes_dev;
-  const uint64_t payload = sb + 10;  // stream | codec u16 = 0 | coded length u64 = 0
+// Kind-1 frame (frame.hpp:3-11, frame.cpp:9-25) with the SPEC.md:282 payload, built
+// from the mask stream:
+//   header | kept_count u32[n_el] | index u32[K] | value f64[K] | codec u16 = 0 |
+//   coded length u64 = 0 | (CRC-32 written afterwards by crc_final_kernel)
+// index = component * P^3 + j (j = kx + P (ky + P kz)), ascending inside the element,
+// so the values keep the stream's order and are one straight copy.  One warp per
+// element for the counts and the indices (a mask word's set bits ranked by popcount,
+// two bits per lane; block value offsets `off` from block_offsets8_kernel), all
+// threads for the value copy (the payload's value array is only 4-byte aligned).
+// n_out = bytes the CRC covers (0 and ISF_STATUS_OVERFLOW when frame_cap is short).
+__global__ void spec_frame_kernel(uint8_t* frame, uint64_t frame_cap, const uint8_t* stream, const uint64_t* off,
+                                  uint64_t n_el, uint32_t E, uint32_t P, uint32_t comps, const uint64_t* kept_dev,
+                                  uint64_t step, double sim_time, uint64_t* n_out, unsigned long long* flags) {
+  const uint64_t K = *kept_dev;
+  const uint64_t payload = 4 * n_el + 12 * K + 10;
   if (48 + payload + 4 > frame_cap) {
-    atomicOr(flags, 4ull);  // ISF_STATUS_OVERFLOW
-    *n_out = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      atomicOr(flags, 4ull);  // ISF_STATUS_OVERFLOW
+      *n_out = 0;
+    }
     return;
   }
-  auto put = [&](uint64_t off, uint64_t v, int nb) {
-    for (int b = 0; b < nb; ++b) frame[off + b] = (uint8_t)(v >> (8 * b));
-  };
-  put(0, 0x31465349ull, 4);  // "ISF1"
-  put(4, 1, 2);              // version
-  put(6, 1, 2);              // payload_kind = CompressedBlock
-  put(8, step, 8);
-  put(16, (uint64_t)__double_as_longlong(sim_time), 8);
-  put(24, E, 4);
-  put(28, P, 4);
-  put(32, comps, 4);
-  put(36, 0, 4);  // reserved
-  put(40, payload, 8);
-  put(48 + sb, 0, 2);      // codec id 0 (no lossless stage)
-  put(48 + sb + 2, 0, 8);  // coded length 0
-  *n_out = 48 + payload;
+  const uint32_t P3 = P * P * P, W = (P3 + 63) / 64;
+  const uint64_t B = n_el * comps;
+  const uint32_t* counts = reinterpret_cast<const uint32_t*>(stream);
+  const uint64_t mask_off = (4 * B + 15) & ~15ull;
+  const uint64_t* masks = reinterpret_cast<const uint64_t*>(stream + mask_off);
+  const uint64_t* vals = reinterpret_cast<const uint64_t*>(stream + mask_off + 8ull * W * B);
+  uint8_t* pl = frame + 48;
+  uint32_t* cnt_out = reinterpret_cast<uint32_t*>(pl);
+  uint32_t* idx_out = reinterpret_cast<uint32_t*>(pl + 4 * n_el);
+  uint32_t* val_out = reinterpret_cast<uint32_t*>(pl + 4 * n_el + 4 * K);
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t p2 = 2 * lane;
+  for (uint64_t e = gw; e < n_el; e += nw) {
+    uint32_t ce = 0;
+    for (uint32_t c = 0; c < comps; ++c) {
+      const uint64_t b = e * comps + c;
+      ce += counts[b];
+      uint64_t base = off[b];
+      for (uint32_t w = 0; w < W; ++w) {
+        const uint64_t m = masks[b * W + w];
+        if (m == 0) continue;  // warp-uniform
+        const uint32_t r0 = (uint32_t)__popcll(m & ((1ull << p2) - 1ull));
+        const uint32_t b0 = (uint32_t)(m >> p2) & 1u, b1 = (uint32_t)(m >> (p2 + 1)) & 1u;
+        const uint32_t j = c * P3 + 64 * w + p2;
+        if (b0) idx_out[base + r0] = j;
+        if (b1) idx_out[base + r0 + b0] = j + 1;
+        base += (uint64_t)__popcll(m);
+      }
+    }
+    if (lane == 0) cnt_out[e] = ce;
+  }
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < K; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = vals[i];
+    val_out[2 * i] = (uint32_t)v;
+    val_out[2 * i + 1] = (uint32_t)(v >> 32);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    auto put = [&](uint64_t o, uint64_t v, int nb) {
+      for (int k = 0; k < nb; ++k) frame[o + k] = (uint8_t)(v >> (8 * k));
+    };
+    put(0, 0x31465349ull, 4);  // "ISF1"
+    put(4, 1, 2);              // version
+    put(6, 1, 2);              // payload_kind = CompressedBlock
+    put(8, step, 8);
+    put(16, (uint64_t)__double_as_longlong(sim_time), 8);
+    put(24, E, 4);
+    put(28, P, 4);
+    put(32, comps, 4);
+    put(36, 0, 4);  // reserved
+    put(40, payload, 8);
+    put(48 + payload - 10, 0, 2);  // codec id 0 (no lossless stage yet)
+    put(48 + payload - 8, 0, 8);   // coded length 0
+    *n_out = 48 + payload;
+  }
 }
 
 }  // namespace crc

@@ -793,24 +793,41 @@ int isf_lossy_crc32(isf_lossy_plan* p, const void* d_data, uint64_t n, uint32_t*
   return crc_launch(p, (const uint8_t*)d_data, nullptr, n, d_crc, nullptr, (cudaStream_t)cuda_stream);
 }
 
-int isf_lossy_frame_async(isf_lossy_plan* p, void* d_frame, uint64_t frame_cap, const isf_lossy_stats* d_stats,
-                          uint32_t elements_per_axis, uint64_t step_index, double sim_time, void* cuda_stream) {
+int isf_lossy_frame_async(isf_lossy_plan* p, void* d_frame, uint64_t frame_cap, const void* d_stream,
+                          uint64_t n_elements, const isf_lossy_stats* d_stats, uint32_t elements_per_axis,
+                          uint64_t step_index, double sim_time, void* cuda_stream) {
   if (int rc = check_plan(p)) return rc;
-  if (!d_frame || !d_stats) return fail(ISF_E_INVALID_ARGUMENT, "null frame or stats pointer");
-  if (((uintptr_t)d_frame & 15u) != 0) return fail(ISF_E_INVALID_ARGUMENT, "frame must be 16-byte aligned");
+  if (!d_frame || !d_stats || !d_stream) return fail(ISF_E_INVALID_ARGUMENT, "null frame, stream or stats pointer");
+  if (((uintptr_t)d_frame & 15u) != 0 || ((uintptr_t)d_stream & 15u) != 0)
+    return fail(ISF_E_INVALID_ARGUMENT, "frame and stream must be 16-byte aligned");
+  if (n_elements == 0) return fail(ISF_E_INVALID_ARGUMENT, "empty field (0 elements)");
   if (frame_cap < ISF_FRAME_OVERHEAD) return fail(ISF_E_LENGTH_MISMATCH, "frame capacity below %d bytes", ISF_FRAME_OVERHEAD);
   DeviceGuard dg(p->device);
   cudaStream_t s = (cudaStream_t)cuda_stream;
   if (!p->crc_n) CUDA_TRY(cudaMalloc(&p->crc_n, 64));
-  isf::crc::frame_header_kernel<<<1, 32, 0, s>>>((uint8_t*)d_frame, frame_cap, &d_stats->stream_bytes,
-                                                 elements_per_axis, p->P, p->comps, step_index, sim_time, p->crc_n,
-                                                 reinterpret_cast<unsigned long long*>(
-                                                     const_cast<uint64_t*>(&d_stats->status)));
+  const uint64_t B = n_elements * p->comps;
+  if (B >= (1ull << 31)) return fail(ISF_E_INVALID_ARGUMENT, "field too large for one call");
+  const uint32_t nchunks = (uint32_t)((B + kOffChunk - 1) / kOffChunk);
+  if (int rc = ensure(p, std::max<uint32_t>(nchunks, 1), 1, B + 1, s)) return rc;
+  // block value offsets of the stream (the same count scan as decompress)
+  Workspace wo{p->status, p->partials, p->counter, p->flags, next_epoch(p, s), nchunks, 0};
+  wo.total_warps = std::min<uint32_t>(nchunks, (uint32_t)p->sms * 4);
+  block_offsets8_kernel<<<wo.total_warps, kOffThreads, 0, s>>>((const uint8_t*)d_stream, B, p->toff, wo,
+                                                                FinalizeArgs{});
+  CUDA_TRY(cudaGetLastError());
+  isf::crc::spec_frame_kernel<<<p->sms * 4, 256, 0, s>>>(
+      (uint8_t*)d_frame, frame_cap, (const uint8_t*)d_stream, p->toff, n_elements, elements_per_axis, p->P, p->comps,
+      &d_stats->kept, step_index, sim_time, p->crc_n,
+      reinterpret_cast<unsigned long long*>(const_cast<uint64_t*>(&d_stats->status)));
   CUDA_TRY(cudaGetLastError());
   if (int rc = crc_launch(p, (const uint8_t*)d_frame, p->crc_n, frame_cap - 4, nullptr, (uint8_t*)d_frame, s))
     return rc;
-  p->last_launches = 3;
+  p->last_launches = 4;
   return 0;
+}
+
+uint64_t isf_lossy_frame_capacity(uint32_t P, uint32_t comps, uint64_t n_elements) {
+  return ISF_FRAME_OVERHEAD + 4 * n_elements + 12 * n_elements * comps * (uint64_t)P * P * P;
 }
 
 }  // extern "C"

@@ -213,29 +213,11 @@ class CompressedBlock:
 
     def spec_payload(self) -> bytes:
         """SPEC.md:282 kind-1 payload: kept_count u32 per element | index u32 | value f64 |
-        codec u16 | coded length u64 | coded bytes (host conversion; indices are
-        (component*P^3 + j) inside the element, derived from the masks)."""
-        host = self.stream.detach().cpu().numpy()
-        P3 = self.points_per_element_axis ** 3
-        B = self.nblocks
-        W = (P3 + 63) // 64
-        m0 = (4 * B + 15) & ~15
-        counts = host[: 4 * B].view(np.uint32)
-        masks = host[m0: m0 + 8 * W * B].view(np.uint64).reshape(B, W)
-        vals = host[m0 + 8 * W * B:].view(np.float64)
-        bits = np.unpackbits(masks.view(np.uint8).reshape(B, W * 8), axis=1, bitorder="little")[:, :P3]
-        bi, ji = np.nonzero(bits)
-        comp = (bi % self.components).astype(np.uint32)
-        idx = comp * np.uint32(P3) + ji.astype(np.uint32)
-        per_el = counts.reshape(self.n_elements, self.components).sum(axis=1).astype(np.uint32)
-        out = bytearray()
-        out += per_el.astype("<u4").tobytes()
-        out += idx.astype("<u4").tobytes()
-        out += vals.astype("<f8").tobytes()
-        out += int(self.lossless_codec).to_bytes(2, "little")
-        out += len(self.coded_bytes).to_bytes(8, "little")
-        out += self.coded_bytes
-        return bytes(out)
+        codec u16 | coded length u64 | coded bytes (indices are component*P^3 + j inside
+        the element, derived from the masks; frame.spec_payload)."""
+        from .frame import spec_payload
+        return spec_payload(self.stream.detach().cpu().numpy(), self.n_elements, self.points_per_element_axis,
+                            self.components, self.lossless_codec, self.coded_bytes)
 
 
 class LossyPlan:
@@ -312,13 +294,18 @@ class LossyPlan:
         _check(self._lib.isf_lossy_crc32(self._h, ctypes.c_void_p(data.data_ptr()), int(nbytes),
                                          ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(cs.cuda_stream)))
 
-    def frame_async(self, frame_buf: torch.Tensor, stats_buf: torch.Tensor, elements_per_axis: int,
-                    step_index: int = 0, sim_time: float = 0.0, cuda_stream=None):
-        """Kind-1 frame around the stream compressed at frame_buf[48:] (stats_buf = that call's stats)."""
+    def frame_async(self, frame_buf: torch.Tensor, stream_buf: torch.Tensor, n_elements: int, stats_buf: torch.Tensor,
+                    elements_per_axis: int, step_index: int = 0, sim_time: float = 0.0, cuda_stream=None):
+        """Kind-1 frame with the SPEC.md:282 payload, converted on the device from the stream
+        in stream_buf (stats_buf = that compress call's stats)."""
         cs = torch.cuda.current_stream(self.device) if cuda_stream is None else cuda_stream
         _check(self._lib.isf_lossy_frame_async(self._h, ctypes.c_void_p(frame_buf.data_ptr()), frame_buf.numel(),
+                                               ctypes.c_void_p(stream_buf.data_ptr()), int(n_elements),
                                                ctypes.c_void_p(stats_buf.data_ptr()), int(elements_per_axis),
                                                int(step_index), float(sim_time), ctypes.c_void_p(cs.cuda_stream)))
+
+    def frame_capacity(self, n_elements: int) -> int:
+        return int(self._lib.isf_lossy_frame_capacity(self.P, self.components, n_elements))
 
     def decompress_async(self, stream_buf: torch.Tensor, stream_bytes: int, n_elements: int,
                          out: torch.Tensor, stats_buf: torch.Tensor, original: torch.Tensor | None = None,
@@ -412,34 +399,35 @@ def lossy_compress(field: Field, cfg: LossyConfig, *, plan: LossyPlan | None = N
 
 def lossy_compress_frame(field: Field, cfg: LossyConfig, step_index: int = 0, sim_time: float = 0.0, *,
                          plan: LossyPlan | None = None):
-    """Compress straight into a staging-ready kind-1 frame on the device:
-    header, stream, codec trailer and CRC-32 are all written by kernels, so the only
-    host work left is one D2H copy of the frame (StageWriter::write_frame,
+    """Compress and build a staging-ready kind-1 frame on the device:
+    the SPEC.md:282 payload (kept_count u32 per element | index u32 | value f64 | codec
+    trailer), header and CRC-32 are all written by kernels, so the only host work left
+    is one D2H copy of the frame (StageWriter::write_frame,
     proj/include/isf/staging/staging.hpp:59-60).  Returns (frame uint8 CUDA tensor of
-    exactly the frame bytes, CompressionReport, kept count)."""
+    exactly the frame bytes, CompressionReport of the stream, kept count)."""
     field.validate_shape()
     v = _device_values(field)
     dev = v.device.index
     plan = plan or get_plan(field.points_per_element_axis, field.components, dev)
     n_el = field.element_count()
-    cap = plan.capacity(n_el) + _native.FRAME_OVERHEAD
-    frame = torch.empty(cap, dtype=torch.uint8, device=v.device)
+    stream = torch.empty(plan.capacity(n_el), dtype=torch.uint8, device=v.device)
+    frame = torch.empty(plan.frame_capacity(n_el), dtype=torch.uint8, device=v.device)
     stats = torch.zeros(12, dtype=torch.float64, device=v.device)
     cs = torch.cuda.current_stream(dev)
     _check(plan._lib.isf_lossy_compress_async(plan.handle, ctypes.c_void_p(v.data_ptr()), n_el,
                                               float(cfg.max_error), int(cfg.error_norm),
-                                              ctypes.c_void_p(frame.data_ptr() + 48), cap - 48,
+                                              ctypes.c_void_p(stream.data_ptr()), stream.numel(),
                                               ctypes.c_void_p(stats.data_ptr()), ctypes.c_void_p(cs.cuda_stream)))
-    plan.frame_async(frame, stats, field.elements_per_axis, step_index, sim_time, cuda_stream=cs)
+    plan.frame_async(frame, stream, n_el, stats, field.elements_per_axis, step_index, sim_time, cuda_stream=cs)
     st = stats.view(torch.int64).cpu()
     status = int(st[10])
     if status & 1:
         raise IsfError(ErrorCode.InvalidArgument, "Field: non-finite value (types.cpp:71-73)")
     if status:
         raise IsfError(ErrorCode.SerializationFailed, f"frame assembly failed (status {status})")
-    sb = int(st[8])
+    sb, kept = int(st[8]), int(st[6])
     rep = CompressionReport.from_sizes(int(st[9]), sb)
-    return frame[: sb + _native.FRAME_OVERHEAD], rep, int(st[6])
+    return frame[: _native.FRAME_OVERHEAD + 4 * n_el + 12 * kept], rep, kept
 
 
 def _decompress(block: CompressedBlock, shape, original: torch.Tensor | None):

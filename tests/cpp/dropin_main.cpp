@@ -37,6 +37,11 @@ int main() {
     auto fr = blk.frame(7, 0.5);
     auto parsed = parse_frame({fr.data(), fr.size()});
     bool ok = parsed.header.kind == PayloadKind::CompressedBlock && parsed.payload.size() == blk.payload().size();
+    // SPEC.md:282 payload: 4 B count per element + 12 B per kept value + codec trailer,
+    // and it parses back to the identical mask stream
+    ok = ok && parsed.payload.size() == 4 * f.element_count() + 12 * blk.kept_total + 10;
+    auto blk2 = tasks::block_from_payload(parsed.payload, parsed.header, f.element_count());
+    ok = ok && blk2.stream == blk.stream && blk2.kept_total == blk.kept_total;
     ok = ok && rep.rel_l2() <= 1e-2 && blk.kept_total <= v.size() / 20;
     bool threw = false;
     try {

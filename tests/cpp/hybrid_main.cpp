@@ -7,7 +7,7 @@
 // run_lossless_suffix): a consumer thread reads the frames with the reference
 // StageReader (its CRC check is the reference's zlib one) and lossless-codes each
 // block's stream on a host thread pool (codec 3, chunked Deflate).  After the timed
-// run every coded block is decoded back into its stream and decompressed against the
+// run every coded block is decoded back (SPEC payload body -> mask stream) and decompressed against the
 // producer's field of that step (exact round trip: the error bound and the stream
 // parser both need every byte).  Prints one JSON line.
 //
@@ -87,9 +87,12 @@ int main(int argc, char** argv) {
     std::vector<double> host_orig(n);
     for (auto& [step, blk] : done) {
         coded_total += blk.coded_bytes.size();
-        // the suffix kept only the coded bytes: decode them back into the block's stream
-        blk.stream = tasks::lossless_decode(blk.coded_bytes, tasks::LosslessCodec(blk.lossless_codec),
-                                            blk.report.compressed_size, threads);
+        // the suffix kept only the coded bytes: decode them back into the SPEC payload body
+        // and that into the block's mask stream
+        const Bytes body = tasks::lossless_decode(blk.coded_bytes, tasks::LosslessCodec(blk.lossless_codec),
+                                                  blk.coded_source_bytes, threads);
+        blk.stream = tasks::detail::stream_from_spec_body(body, n_el, P, 1);
+        if (blk.stream.size() != blk.report.compressed_size) ok = false;
         isf_lossy_generate_tgv(gen, d_field, E, 0, E, int(step % 4), 2 * M_PI, nullptr);
         cudaMemcpy(host_orig.data(), d_field, n * 8, cudaMemcpyDeviceToHost);
         Field orig(E, P, 1, host_orig);

@@ -49,16 +49,20 @@ def _ref_frame(L, h, payload: bytes) -> bytes:
 def test_kind1_frame_bytes_equal_reference(ref, oracle):
     u = oracle.gen_tgv(4, 8, 0)
     rc, s, st = oracle.compress(u, 8, 1, 1e-3)
-    payload = FR.block_payload(s.tobytes())
+    payload = FR.spec_payload(s, 64, 8, 1)
     h = FR.FrameHeader(FR.KIND_COMPRESSED_BLOCK, 42, 0.125, 4, 8, 1, len(payload))
     mine = FR.build_frame(h, payload)
     assert mine == _ref_frame(ref, h, payload)
     off, ln, kind = ctypes.c_ulonglong(), ctypes.c_ulonglong(), ctypes.c_uint()
     assert ref.ref_parse_frame(mine, len(mine), ctypes.byref(off), ctypes.byref(ln), ctypes.byref(kind)) == 0
     assert kind.value == 1 and off.value == 48 and ln.value == len(payload)
-    hh, pl = FR.parse_frame(mine)
-    stream, codec, coded = FR.split_block_payload(pl, len(s))
+    hh, stream, codec, coded = FR.parse_block_frame(mine)
     assert stream == s.tobytes() and codec == 0 and coded == b""
+    # SPEC.md:282 layout: kept_count u32 per element | index u32 | value f64 | trailer
+    K = int(st.kept)
+    assert len(payload) == 4 * 64 + 12 * K + 10
+    per_el = np.frombuffer(payload, dtype="<u4", count=64)
+    assert int(per_el.sum()) == K
 
 
 def test_crc_and_error_codes_match_reference(ref):

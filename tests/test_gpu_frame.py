@@ -38,6 +38,8 @@ def test_crc32_large_chunk_tree(native):
 
 @pytest.mark.parametrize("which,eps", [(0, 1e-3), (2, 1e-3), (3, 1e-5)])
 def test_device_frame_equals_host_frame(native, oracle, which, eps):
+    """The device frame (SPEC.md:282 payload converted on the device) equals the host
+    framing of the oracle's stream, and parses back to exactly that stream."""
     import paper_2407_20731_b200 as PK
     from paper_2407_20731_b200 import frame as FR
     E, P = 8, 8
@@ -47,12 +49,28 @@ def test_device_frame_equals_host_frame(native, oracle, which, eps):
     got = fr.cpu().numpy().tobytes()
     rc, ref, _ = oracle.compress(u, P, 1, eps)
     assert rc == 0
-    want = FR.build_frame(FR.FrameHeader(FR.KIND_COMPRESSED_BLOCK, 42, 0.125, E, P, 1),
-                          FR.block_payload(ref.tobytes()))
+    payload = FR.spec_payload(ref, E ** 3, P, 1)
+    want = FR.build_frame(FR.FrameHeader(FR.KIND_COMPRESSED_BLOCK, 42, 0.125, E, P, 1), payload)
     assert got == want
-    h, payload = FR.parse_frame(got)
-    assert h.payload_len == len(ref) + 10 and payload[: len(ref)] == ref.tobytes()
+    h, stream, codec, coded = FR.parse_block_frame(got)
+    assert stream == ref.tobytes() and codec == 0 and coded == b""
+    assert h.payload_len == 4 * E ** 3 + 12 * kept + 10
     assert rep.compressed_size == len(ref)
+
+
+@pytest.mark.parametrize("P,comps,n", [(6, 1, 27), (8, 3, 8), (12, 1, 8)])
+def test_device_frame_generic_lx_and_vector(native, oracle, P, comps, n):
+    import paper_2407_20731_b200 as PK
+    from paper_2407_20731_b200 import frame as FR
+    u = np.random.default_rng(P * comps).standard_normal(n * P ** 3 * comps)
+    E = round(n ** (1 / 3))
+    f = PK.Field(E, P, comps, torch.from_numpy(u).cuda())
+    fr, rep, kept = PK.lossy_compress_frame(f, PK.LossyConfig(1e-2))
+    rc, ref, _ = oracle.compress(u, P, comps, 1e-2)
+    got = fr.cpu().numpy().tobytes()
+    assert got == FR.build_frame(FR.FrameHeader(FR.KIND_COMPRESSED_BLOCK, 0, 0.0, E, P, comps),
+                                 FR.spec_payload(ref, n, P, comps))
+    assert FR.parse_block_frame(got, n)[1] == ref.tobytes()
 
 
 def test_device_frame_overflow_flag(native, oracle):
@@ -61,11 +79,10 @@ def test_device_frame_overflow_flag(native, oracle):
     u = oracle.gen_tgv(E, P, 0)
     plan = PK.get_plan(P, 1, 0)
     n_el = E ** 3
-    cap = plan.capacity(n_el)
-    frame = torch.zeros(cap + 64, dtype=torch.uint8, device="cuda")
+    stream = torch.zeros(plan.capacity(n_el), dtype=torch.uint8, device="cuda")
     stats = torch.zeros(12, dtype=torch.float64, device="cuda")
-    plan.compress_async(torch.from_numpy(u).cuda(), n_el, 1e-3, frame[48:], stats)
-    small = frame[: 64]   # far too small for header + stream + trailer
-    plan.frame_async(small, stats, E)
+    plan.compress_async(torch.from_numpy(u).cuda(), n_el, 1e-3, stream, stats)
+    small = torch.zeros(64, dtype=torch.uint8, device="cuda")  # far too small for header + payload
+    plan.frame_async(small, stream, n_el, stats, E)
     torch.cuda.synchronize()
     assert int(stats.view(torch.int64)[10].item()) & 4
