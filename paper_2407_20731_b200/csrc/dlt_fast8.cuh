@@ -741,7 +741,25 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       v[2 * z] = t.x;
       v[2 * z + 1] = t.y;
     }
+    // all-zero block (+-0 only): its coefficients are all zero, so it keeps nothing
+    // -- skip the transform and the selection.  NaN / Inf / subnormal
+    // bits are non-zero and take the normal path.
+    uint32_t zlo = 0, zhi = 0;
+#pragma unroll
+    for (int r = 0; r < 16; r += 2) {
+      zlo |= (uint32_t)__double2loint(v[r]) | (uint32_t)__double2loint(v[r + 1]);
+      zhi |= (uint32_t)__double2hiint(v[r]) | (uint32_t)__double2hiint(v[r + 1]);
+    }
+    const bool zblk = !__any_sync(0xffffffffu, (zlo | (zhi & 0x7fffffffu)) != 0u);
     __syncwarp();
+    if (zblk) {
+      fence_proxy_async();
+      __syncwarp();
+      issue(blk + kC8Stages * W, st);
+      st = (st + 1 == kC8Stages) ? 0 : st + 1;
+      if (lane == 0) counts[blk] = 0u;
+      masks16[blk * 32 + lane] = (uint16_t)0;
+    } else {
 #ifndef ISF_EXP_NOXFORM
     lines8<0, 2, 0, 1, 2, false>(v);  // z sweep
 #endif
@@ -849,6 +867,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
       }
     }
     (void)off;
+    }  // non-zero block
     }  // live block
     if constexpr (SP) {
       // this CTA's aggregate of round it: the last of its 16 warps publishes it

@@ -49,8 +49,10 @@ for which in (range(1) if os.environ.get("TK_ONLY_U") else range(4)):
     torch.cuda.synchronize()
     tc += e0.elapsed_time(e1) / K
     td += e1.elapsed_time(e2) / K
+    res["uvwp"[which]] = [round(e0.elapsed_time(e1) / K, 4), round(e1.elapsed_time(e2) / K, 4)]
 F = (1 if os.environ.get("TK_ONLY_U") else 4) * n * 4096
-print(json.dumps({"compress_gbs": F / tc / 1e6, "decompress_gbs": F / td / 1e6, "field_gbs": F / (tc + td) / 1e6}))
+print(json.dumps({"compress_gbs": F / tc / 1e6, "decompress_gbs": F / td / 1e6, "field_gbs": F / (tc + td) / 1e6,
+                  "ms_c_d": res}))
 '''
 
 for lib in sys.argv[1:]:
