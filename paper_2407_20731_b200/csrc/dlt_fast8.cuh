@@ -648,7 +648,22 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   const uint32_t tx = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (SP ? 128u : 64u) * (uint32_t)(warp >> 2);
   const uint32_t wbase_a = smem_u32(wbase), bars_a = smem_u32(bars);  // hoisted shared-window addresses
   const uint64_t pol_stream = l2_policy_evict_first();  // the field is read once
+  // vector fields (components = 3, element -> point -> component): a block is every
+  // third double of its element, so each lane gathers 16 of them with 8-byte cp.async
+  // into the same dense stage the TMA engine fills for scalar fields (one commit group
+  // per stage, empty past the end so the group count stays in step)
+  const bool vec = A.comps == 3;
   auto issue = [&](uint64_t blk, int st) {
+    if (vec) {
+      if (blk < B) {
+        const double* src = A.field + (blk / 3) * 1536 + (blk % 3);
+        const uint32_t dst = wbase_a + (uint32_t)(st * kC8Stage);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) cp_async8(dst + 8u * (uint32_t)(lane + 32 * k), src + 3 * (lane + 32 * k));
+      }
+      cp_async_commit();
+      return;
+    }
     if (lane == 0 && blk < B) {
       mbar_arrive_tx_a(bars_a + 8u * st, 4096u);
       bulk_g2s_hint_a(wbase_a + (uint32_t)(st * kC8Stage), A.field + blk * 512, 4096u, bars_a + 8u * st, pol_stream);
@@ -731,8 +746,14 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     uint32_t mask = 0, kept = 0;
     if (!SP || blk < B) {  // warp-uniform
     double2* sb = reinterpret_cast<double2*>(wbase + st * kC8Stage);
-    mbar_wait_a(bars_a + 8u * st, (ph >> st) & 1u);
-    ph ^= 1u << st;
+    if (vec) {
+      static_assert(kC8Stages == 2, "one group in flight behind the consumed stage");
+      cp_async_wait<1>();
+      __syncwarp();
+    } else {
+      mbar_wait_a(bars_a + 8u * st, (ph >> st) & 1u);
+      ph ^= 1u << st;
+    }
     double v[16];
     // z-lines: lane = (y = l/4, q = l%4) holds x = 2q, 2q+1 of row y for all z
 #pragma unroll
@@ -1239,6 +1260,13 @@ constexpr int kD8StageBytes = (kD8Stage + 127) & ~127;
 constexpr int kD8WarpBytes = kF8Stages * kD8StageBytes + 128;  // stages | mbarriers
 template <bool ERR>
 __host__ __device__ constexpr int d8_smem() { return d8_warps<ERR>() * kD8WarpBytes; }
+// vector fields (components = 3): 15 warps per CTA = the 3 components of 5 elements per
+// round, reconstructed into a shared-memory copy of those elements (point-major,
+// component-minor) and written out with coalesced 128-bit stores (12 warps with a
+// double buffer and one barrier per round measured 7 % slower: fewer warps)
+constexpr int kD8VecWarps = 15;
+constexpr int kD8VecElems = kD8VecWarps / 3;
+constexpr int d8_vec_smem() { return kD8VecWarps * kD8WarpBytes + kD8VecElems * 1536 * 8; }
 
 struct Decompress8Args {
   DecompressArgs d;
@@ -1248,9 +1276,10 @@ struct Decompress8Args {
 
 // ERR: also read the original and accumulate the error report (separate instantiation
 // so the plain decode does not carry the accumulators' registers)
-template <bool ERR>
-__global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decompress8Args P) {
-  constexpr int kNW = d8_warps<ERR>();
+template <bool ERR, bool VEC = false>
+__global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) decompress8_kernel(Decompress8Args P) {
+  constexpr int kNW = VEC ? kD8VecWarps : d8_warps<ERR>();
+  static_assert(!(VEC && ERR), "the error report of vector fields takes the strided path");
   const DecompressArgs& A = P.d;
   extern __shared__ __align__(128) unsigned char smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1304,7 +1333,11 @@ __global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decom
   issue(gw + W, 1, p0, p1);
   int st = 0;
   uint32_t ph = 0;
-  for (uint64_t blk = gw; blk < B; blk += W) {
+  // VEC: every warp runs every round (the CTA writes its 5 elements after a barrier)
+  double* obuf = reinterpret_cast<double*>(smem + kNW * kD8WarpBytes);
+  const uint64_t nrounds = VEC ? (B + W - 1) / W : 0;
+  for (uint64_t it = 0, blk = gw; VEC ? it < nrounds : blk < B; ++it, blk += W) {
+    if (!VEC || blk < B) {
     unsigned char* sp = wbase + st * kD8StageBytes;
     uint64_t r0 = 0, r1 = 0;  // offsets / mask of blk + 2W, consumed by the refill below
     uint32_t mr = 0;
@@ -1469,14 +1502,34 @@ __global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decom
     if (lowz) inv2_low8<2, 0, 1, 2>(v); else lines8<2, 2, 0, 1, 2, true>(v);  // inverse z sweep
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = __dadd_rn(v[r], 0.0);  // zeros as +0
-    double2* dst = reinterpret_cast<double2*>(A.out + blk * 512) + lane;
-#pragma unroll
-    for (int z = 0; z < 8; ++z) stg_stream(dst + z * 32, make_double2(v[2 * z], v[2 * z + 1]));
-    if (ERR) {
-      const double2* src = reinterpret_cast<const double2*>(A.orig + blk * 512) + lane;
+    const bool vec = A.comps == 3;  // vector field: the block is every third double of its element
+    if constexpr (VEC) {
+      // element warp / 3 of the CTA's round, component warp % 3 (the round's first block
+      // is a multiple of 3: 15 blocks per CTA, 15 x grid per round)
+      double* ov = obuf + (warp / 3) * 1536 + (warp % 3) + 3 * (2 * q + 8 * y);
 #pragma unroll
       for (int z = 0; z < 8; ++z) {
-        const double2 o = ldg_stream(src + z * 32);
+        ov[192 * z] = v[2 * z];
+        ov[192 * z + 3] = v[2 * z + 1];
+      }
+    } else if (vec) {
+      double* dv = A.out + (blk / 3) * 1536 + (blk % 3) + 3 * (2 * q + 8 * y);
+#pragma unroll
+      for (int z = 0; z < 8; ++z) {  // plain stores: L2 merges the three components' sectors
+        dv[192 * z] = v[2 * z];
+        dv[192 * z + 3] = v[2 * z + 1];
+      }
+    } else {
+      double2* dst = reinterpret_cast<double2*>(A.out + blk * 512) + lane;
+#pragma unroll
+      for (int z = 0; z < 8; ++z) stg_stream(dst + z * 32, make_double2(v[2 * z], v[2 * z + 1]));
+    }
+    if (ERR) {
+      const double2* src = reinterpret_cast<const double2*>(A.orig + blk * 512) + lane;
+      const double* sv3 = A.orig + (blk / 3) * 1536 + (blk % 3) + 3 * (2 * q + 8 * y);
+#pragma unroll
+      for (int z = 0; z < 8; ++z) {
+        const double2 o = vec ? make_double2(__ldcs(sv3 + 192 * z), __ldcs(sv3 + 192 * z + 3)) : ldg_stream(src + z * 32);
         const double wz = Wg<8>(z);
         const double w0 = __dmul_rn(wxy0, wz), w1 = __dmul_rn(wxy1, wz);
         const double da = __dsub_rn(o.x, v[2 * z]), db = __dsub_rn(o.y, v[2 * z + 1]);
@@ -1490,6 +1543,17 @@ __global__ void __launch_bounds__(d8_warps<ERR>() * 32) decompress8_kernel(Decom
         t = abs_bits(o.x); uinf = t > uinf ? t : uinf;
         t = abs_bits(o.y); uinf = t > uinf ? t : uinf;
       }
+    }
+    }  // live block
+    if constexpr (VEC) {
+      __syncthreads();  // the round's 5 elements are in obuf
+      const uint64_t e0 = (blockIdx.x * (uint64_t)kNW + it * W) / 3;
+      const uint64_t nel = B / 3;
+      const uint64_t ne = e0 >= nel ? 0 : (nel - e0 < (uint64_t)kD8VecElems ? nel - e0 : (uint64_t)kD8VecElems);
+      const double2* src = reinterpret_cast<const double2*>(obuf);
+      double2* dst = reinterpret_cast<double2*>(A.out + e0 * 1536);
+      for (uint32_t i = threadIdx.x; i < ne * 768; i += kNW * 32) stg_stream(dst + i, src[i]);
+      __syncthreads();  // obuf is free for the next round
     }
   }
   if (ERR) {

@@ -119,6 +119,7 @@ struct isf_lossy_plan {
   uint64_t* rstat = nullptr;  // single-pass compress: [round][cta] epoch-tagged aggregates
   size_t rstat_cap = 0;
   bool use_sp = false;        // single-pass compress8 (isf_lossy_plan_set_compress_mode)
+  int grid8dv = 0;            // decompress8 for vector fields (components = 3)
   size_t status_cap = 0;
   double* partials = nullptr;
   size_t partials_cap = 0;  // slots of 4 doubles
@@ -291,7 +292,7 @@ int dispatch_decompress_generic(LxList<L0, Ls...>, int lx, isf_lossy_plan* p, co
 }
 using AllLx = LxList<2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>;
 
-bool use_fast8(const isf_lossy_plan* p) { return p->P == 8 && p->comps == 1; }
+bool use_fast8(const isf_lossy_plan* p) { return p->P == 8 && (p->comps == 1 || p->comps == 3); }
 
 int check_plan(const isf_lossy_plan* p) {
   if (!p) return fail(ISF_E_INVALID_ARGUMENT, "null plan");
@@ -390,6 +391,13 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel<true>, d8_warps<true>() * 32,
                                                            d8_smem<true>()));
     p->grid8de = p->sms * std::max(occ, 1);
+    if (p->comps == 3) {
+      CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    d8_vec_smem()));
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel<false, true>, kD8VecWarps * 32,
+                                                             d8_vec_smem()));
+      p->grid8dv = p->sms * std::max(occ, 1);
+    }
   }
   CUDA_TRY(ensure(p, 1 << 16, 1 << 14, 1 << 16, 0) == 0 ? cudaSuccess : cudaErrorMemoryAllocation);
   // the zeroing above ran on the legacy stream: complete it before any caller stream
@@ -643,8 +651,10 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
     CUDA_TRY(launch_pdl(block_offsets8_kernel, wo.total_warps, kOffThreads, 0, s, (const uint8_t*)d_stream, B, p->toff,
                         wo, FinalizeArgs{}));
     CUDA_TRY(cudaGetLastError());
-    const int nw = d_original ? kD8WarpsErr : kD8Warps;
-    grid = (uint32_t)std::min<uint64_t>((uint64_t)(d_original ? p->grid8de : p->grid8d), (B + nw - 1) / nw);
+    const bool vec = p->comps == 3 && !d_original;
+    const int nw = d_original ? kD8WarpsErr : (vec ? kD8VecWarps : kD8Warps);
+    grid = (uint32_t)std::min<uint64_t>((uint64_t)(d_original ? p->grid8de : (vec ? p->grid8dv : p->grid8d)),
+                                        (B + nw - 1) / nw);
     a.ws.total_warps = grid * nw;
     parts = grid * nw;
     FinalizeArgs f{1, p->partials, d_original ? parts : 0u, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
@@ -652,6 +662,8 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
     Decompress8Args a8{a, p->toff, f};
     if (d_original)  // + error report and fused finalize
       CUDA_TRY(launch_pdl(decompress8_kernel<true>, grid, d8_warps<true>() * 32, d8_smem<true>(), s, a8));
+    else if (vec)
+      CUDA_TRY(launch_pdl(decompress8_kernel<false, true>, grid, kD8VecWarps * 32, d8_vec_smem(), s, a8));
     else
       CUDA_TRY(launch_pdl(decompress8_kernel<false>, grid, d8_warps<false>() * 32, d8_smem<false>(), s, a8));
     CUDA_TRY(cudaGetLastError());

@@ -131,6 +131,23 @@ def test_vector_field_components3(native, oracle):
     assert np.linalg.norm(back.values.cpu().numpy() - ob) <= REL_TOL * np.linalg.norm(ob)
 
 
+@pytest.mark.parametrize("eps,n_el", [(1e-2, 1000), (1e-5, 1000), (1e-3, 37)])
+def test_vector_field_fast_path(native, oracle, eps, n_el):
+    """components = 3 at lx = 8 runs on compress8 / compact8 / decompress8 (the stride-3
+    block gather by cp.async): streams, reconstructions and the error report match the
+    oracle exactly."""
+    import paper_2407_20731_b200 as PK
+    blocks = oracle.gen_spectral(8, 3 * n_el, block0=5).reshape(n_el, 3, 512)
+    vals = np.ascontiguousarray(blocks.transpose(0, 2, 1)).reshape(-1)  # element -> point -> component
+    f, blk, ref, st = _compress_both(native, oracle, vals, 8, 3, eps)
+    assert PK.get_plan(8, 3, 0).last_launches() == 2          # compress8 + compact8
+    assert _assert_stream_parity(oracle, blk, ref, 8, 3, eps) == 0
+    back, rep = native.decompress_with_error(blk, f.shape, f)
+    rc, ob, ost = oracle.decompress(ref, 8, 3, n_el, original=vals)
+    assert rc == 0 and np.array_equal(back.values.cpu().numpy(), ob)  # bit-identical
+    assert abs(rep.err2 - ost.err2) <= 1e-9 * max(ost.err2, 1e-300) and rep.err_inf == ost.err_inf
+
+
 @pytest.mark.parametrize("n_el", [1, 3, 5, 7, 9, 33])
 def test_ragged_small(native, oracle, n_el):
     u = oracle.gen_spectral(8, n_el, block0=77)
