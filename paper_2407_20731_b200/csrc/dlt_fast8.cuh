@@ -610,7 +610,7 @@ struct Sp8Args {
   FinalizeArgs fin;
 };
 
-template <bool SP>
+template <bool SP, bool VEC = false>
 __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A, Sp8Args S) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t s_tmem;
@@ -652,9 +652,8 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
   // third double of its element, so each lane gathers 16 of them with 8-byte cp.async
   // into the same dense stage the TMA engine fills for scalar fields (one commit group
   // per stage, empty past the end so the group count stays in step)
-  const bool vec = A.comps == 3;
   auto issue = [&](uint64_t blk, int st) {
-    if (vec) {
+    if constexpr (VEC) {
       if (blk < B) {
         const double* src = A.field + (blk / 3) * 1536 + (blk % 3);
         const uint32_t dst = wbase_a + (uint32_t)(st * kC8Stage);
@@ -746,7 +745,7 @@ __global__ void __launch_bounds__(kC8Warps * 32) compress8_kernel(CompressArgs A
     uint32_t mask = 0, kept = 0;
     if (!SP || blk < B) {  // warp-uniform
     double2* sb = reinterpret_cast<double2*>(wbase + st * kC8Stage);
-    if (vec) {
+    if constexpr (VEC) {
       static_assert(kC8Stages == 2, "one group in flight behind the consumed stage");
       cp_async_wait<1>();
       __syncwarp();
@@ -1502,7 +1501,9 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
     if (lowz) inv2_low8<2, 0, 1, 2>(v); else lines8<2, 2, 0, 1, 2, true>(v);  // inverse z sweep
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = __dadd_rn(v[r], 0.0);  // zeros as +0
-    const bool vec = A.comps == 3;  // vector field: the block is every third double of its element
+    // vector field (the block is every third double of its element): VEC stages the
+    // CTA's elements in shared memory; the error-report instantiation stores strided
+    const bool vec = ERR && A.comps == 3;
     if constexpr (VEC) {
       // element warp / 3 of the CTA's round, component warp % 3 (the round's first block
       // is a multiple of 3: 15 blocks per CTA, 15 x grid per round)

@@ -378,6 +378,12 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
     CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   d8_smem<true>()));
     CUDA_TRY(cudaFuncSetAttribute(compress8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
+    if (p->comps == 3) {  // vector fields: the cp.async-gather instantiations
+      CUDA_TRY(cudaFuncSetAttribute(compress8_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kC8Smem));
+      CUDA_TRY(cudaFuncSetAttribute(compress8_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kC8Smem));
+    }
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel<true>, kC8Warps * 32, kC8Smem));
     p->grid8c = p->sms * std::max(occ, 1);
@@ -514,7 +520,9 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
       }
       Sp8Args sp{p->rstat, a.ws.epoch, nrounds, reinterpret_cast<double*>(a.stream + a.val_off), cap_vals,
                  p->toff + B, f};
-      const cudaError_t le = launch_coop_pdl(compress8_kernel<true>, grid, kC8Warps * 32, kC8Smem, s, a, sp);
+      const cudaError_t le =
+          p->comps == 3 ? launch_coop_pdl(compress8_kernel<true, true>, grid, kC8Warps * 32, kC8Smem, s, a, sp)
+                        : launch_coop_pdl(compress8_kernel<true>, grid, kC8Warps * 32, kC8Smem, s, a, sp);
       if (le == cudaSuccess) {
         p->last_launches = 1;
         return 0;
@@ -532,7 +540,10 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
       p->vslot_cap = slot_bytes;
     }
     a.vslot = p->vslot;
-    CUDA_TRY(launch_pdl(compress8_kernel<false>, grid, kC8Warps * 32, kC8Smem, s, a, Sp8Args{}));
+    if (p->comps == 3)
+      CUDA_TRY(launch_pdl(compress8_kernel<false, true>, grid, kC8Warps * 32, kC8Smem, s, a, Sp8Args{}));
+    else
+      CUDA_TRY(launch_pdl(compress8_kernel<false>, grid, kC8Warps * 32, kC8Smem, s, a, Sp8Args{}));
     CUDA_TRY(launch_pdl(compact8_kernel, nchunks8 + 1, kCompactThreads, 0, s, a.stream, B, a.mask_off,
                         (const uint64_t*)a.ws.csum, p->csum + (p->csum_par ^ 1) * p->status_cap,
                         (const double*)p->vslot, reinterpret_cast<double*>(a.stream + a.val_off), cap_vals,
