@@ -468,12 +468,23 @@ __global__ void __launch_bounds__(gen_dthreads<LX>()) decompress_generic(Decompr
     __syncthreads();
     const uint64_t prefix = misc[1];
     const bool bad = misc[2] != 0;
-    for (int p = tid; p < N3; p += kT) {
-      const uint64_t mw = maskw[p >> 6];
-      double val = 0.0;
-      if (!bad && ((mw >> (p & 63)) & 1ull))
-        val = vals[prefix + wpre[p >> 6] + __popcll(mw & ((1ull << (p & 63)) - 1ull))];
-      u[p] = val;
+    // the gather's global loads are independent: batches of 8 in flight per thread
+    constexpr int kG = 8;
+    for (int p0 = tid; p0 < N3; p0 += kG * kT) {
+      double val[kG];
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        const int p = p0 + g * kT;
+        val[g] = 0.0;
+        if (p < N3) {
+          const uint64_t mw = maskw[p >> 6];
+          if (!bad && ((mw >> (p & 63)) & 1ull))
+            val[g] = vals[prefix + wpre[p >> 6] + __popcll(mw & ((1ull << (p & 63)) - 1ull))];
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < kG; ++g)
+        if (p0 + g * kT < N3) u[p0 + g * kT] = val[g];
     }
     __syncthreads();
     for (int l = tid; l < N2; l += kT) inv_line_ptr<LX>(u + l * N, 1);                     // x
