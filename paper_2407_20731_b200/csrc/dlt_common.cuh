@@ -351,10 +351,31 @@ __device__ __forceinline__ void radix_select(const LaneGroup<G>& g, const Src& s
     const uint64_t nhi_full = nlo + ((1ull << shift) - 1);
     const uint64_t nhi = nhi_full < khi ? nhi_full : khi;
     uint64_t mn = ~0ull, mx = 0;
-    for (int p = g.rank; p < n; p += G) {
-      uint64_t k; uint32_t ix;
-      src(p, k, ix);
-      if (k >= nlo && k <= nhi) { mn = k < mn ? k : mn; mx = k > mx ? k : mx; }
+    if constexpr (Src::kCompact && G == 32) {
+      // keep only the candidates of the cut bin (in place: a chunk's survivors land at
+      // or before the chunk), so the next passes scan the survivors alone
+      int w = 0;
+      for (int p0 = 0; p0 < n; p0 += 32) {
+        const int p = p0 + g.rank;
+        uint64_t k = 0; uint32_t ix = 0;
+        if (p < n) src(p, k, ix);
+        const bool keep = p < n && k >= nlo && k <= nhi;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          src.set(w + __popc(bal & ((1u << g.rank) - 1u)), ix);
+          mn = k < mn ? k : mn;
+          mx = k > mx ? k : mx;
+        }
+        w += __popc(bal);
+      }
+      n = w;
+      __syncwarp();
+    } else {
+      for (int p = g.rank; p < n; p += G) {
+        uint64_t k; uint32_t ix;
+        src(p, k, ix);
+        if (k >= nlo && k <= nhi) { mn = k < mn ? k : mn; mx = k > mx ? k : mx; }
+      }
     }
     klo = g.min(mn);
     khi = g.max(mx);
@@ -461,10 +482,31 @@ __device__ void radix_select_w(const LaneGroup<G>& g, const Src& src, const Wt& 
     const uint64_t nhi_full = nlo + ((1ull << shift) - 1);
     const uint64_t nhi = nhi_full < khi ? nhi_full : khi;
     uint64_t mn = ~0ull, mx = 0;
-    for (int p = g.rank; p < n; p += G) {
-      uint64_t k; uint32_t ix;
-      src(p, k, ix);
-      if (k >= nlo && k <= nhi) { mn = k < mn ? k : mn; mx = k > mx ? k : mx; }
+    if constexpr (Src::kCompact && G == 32) {
+      // keep only the candidates of the cut bin (in place: a chunk's survivors land at
+      // or before the chunk), so the next passes scan the survivors alone
+      int w = 0;
+      for (int p0 = 0; p0 < n; p0 += 32) {
+        const int p = p0 + g.rank;
+        uint64_t k = 0; uint32_t ix = 0;
+        if (p < n) src(p, k, ix);
+        const bool keep = p < n && k >= nlo && k <= nhi;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          src.set(w + __popc(bal & ((1u << g.rank) - 1u)), ix);
+          mn = k < mn ? k : mn;
+          mx = k > mx ? k : mx;
+        }
+        w += __popc(bal);
+      }
+      n = w;
+      __syncwarp();
+    } else {
+      for (int p = g.rank; p < n; p += G) {
+        uint64_t k; uint32_t ix;
+        src(p, k, ix);
+        if (k >= nlo && k <= nhi) { mn = k < mn ? k : mn; mx = k > mx ? k : mx; }
+      }
     }
     klo = g.min(mn);
     khi = g.max(mx);
@@ -473,11 +515,14 @@ __device__ void radix_select_w(const LaneGroup<G>& g, const Src& src, const Wt& 
 
 // element sources for radix_select
 struct SrcIndirect {  // candidate indices into the block's coefficients (generic kernels)
+  static constexpr bool kCompact = true;  // radix_select narrows the list in place
   const double* a;
-  const uint16_t* idxs;
+  uint16_t* idxs;
   __device__ __forceinline__ void operator()(int p, uint64_t& k, uint32_t& ix) const { ix = idxs[p]; k = abs_bits(a[ix]); }
+  __device__ __forceinline__ void set(int p, uint32_t ix) const { idxs[p] = (uint16_t)ix; }
 };
 struct SrcDense {  // raw coefficients in natural order, index = position (fast kernels)
+  static constexpr bool kCompact = false;
   const double* a;
   __device__ __forceinline__ void operator()(int p, uint64_t& k, uint32_t& ix) const { k = abs_bits(a[p]); ix = (uint32_t)p; }
 };
