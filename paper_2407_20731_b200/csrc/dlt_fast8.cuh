@@ -1547,14 +1547,20 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
     }
     }  // live block
     if constexpr (VEC) {
-      __syncthreads();  // the round's 5 elements are in obuf
-      const uint64_t e0 = (blockIdx.x * (uint64_t)kNW + it * W) / 3;
-      const uint64_t nel = B / 3;
-      const uint64_t ne = e0 >= nel ? 0 : (nel - e0 < (uint64_t)kD8VecElems ? nel - e0 : (uint64_t)kD8VecElems);
-      const double2* src = reinterpret_cast<const double2*>(obuf);
-      double2* dst = reinterpret_cast<double2*>(A.out + e0 * 1536);
-      for (uint32_t i = threadIdx.x; i < ne * 768; i += kNW * 32) stg_stream(dst + i, src[i]);
-      __syncthreads();  // obuf is free for the next round
+      // the 3 warps of element warp / 3 meet on their own named barrier (96 threads), so
+      // elements proceed independently: the element is in obuf -> its 12 KiB go out with
+      // 128-bit stores by those 96 threads -> the buffer is free for the next round
+      const uint32_t le = (uint32_t)warp / 3u;
+      const uint64_t e = (blockIdx.x * (uint64_t)kNW + it * W) / 3 + le;
+      asm volatile("bar.sync %0, 96;" ::"r"(1u + le) : "memory");
+      if (e < B / 3) {
+        const double2* src = reinterpret_cast<const double2*>(obuf + le * 1536);
+        double2* dst = reinterpret_cast<double2*>(A.out + e * 1536);
+        const uint32_t t = (uint32_t)(warp % 3) * 32u + (uint32_t)lane;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) stg_stream(dst + t + 96 * i, src[t + 96 * i]);
+      }
+      asm volatile("bar.sync %0, 96;" ::"r"(1u + le) : "memory");
     }
   }
   if (ERR) {
