@@ -1263,9 +1263,13 @@ __host__ __device__ constexpr int d8_smem() { return d8_warps<ERR>() * kD8WarpBy
 // round, reconstructed into a shared-memory copy of those elements (point-major,
 // component-minor) and written out with coalesced 128-bit stores (12 warps with a
 // double buffer and one barrier per round measured 7 % slower: fewer warps)
-constexpr int kD8VecWarps = 15;
+#ifndef ISF_D8V_WARPS
+#define ISF_D8V_WARPS 15
+#endif
+constexpr int kD8VecWarps = ISF_D8V_WARPS;
 constexpr int kD8VecElems = kD8VecWarps / 3;
-constexpr int d8_vec_smem() { return kD8VecWarps * kD8WarpBytes + kD8VecElems * 1536 * 8; }
+constexpr int kD8VecBufs = kD8VecWarps <= 12 ? 2 : 1;  // element buffers per element (double buffer if it fits)
+constexpr int d8_vec_smem() { return kD8VecWarps * kD8WarpBytes + kD8VecBufs * kD8VecElems * 1536 * 8; }
 
 struct Decompress8Args {
   DecompressArgs d;
@@ -1507,7 +1511,7 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
     if constexpr (VEC) {
       // element warp / 3 of the CTA's round, component warp % 3 (the round's first block
       // is a multiple of 3: 15 blocks per CTA, 15 x grid per round)
-      double* ov = obuf + (warp / 3) * 1536 + (warp % 3) + 3 * (2 * q + 8 * y);
+      double* ov = obuf + ((kD8VecBufs == 2 ? (it & 1) * kD8VecElems : 0) + warp / 3) * 1536 + (warp % 3) + 3 * (2 * q + 8 * y);
 #pragma unroll
       for (int z = 0; z < 8; ++z) {
         ov[192 * z] = v[2 * z];
@@ -1554,13 +1558,16 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
       const uint64_t e = (blockIdx.x * (uint64_t)kNW + it * W) / 3 + le;
       asm volatile("bar.sync %0, 96;" ::"r"(1u + le) : "memory");
       if (e < B / 3) {
-        const double2* src = reinterpret_cast<const double2*>(obuf + le * 1536);
+        const double2* src = reinterpret_cast<const double2*>(
+            obuf + ((kD8VecBufs == 2 ? (it & 1) * kD8VecElems : 0) + le) * 1536);
         double2* dst = reinterpret_cast<double2*>(A.out + e * 1536);
         const uint32_t t = (uint32_t)(warp % 3) * 32u + (uint32_t)lane;
 #pragma unroll
         for (int i = 0; i < 8; ++i) stg_stream(dst + t + 96 * i, src[t + 96 * i]);
       }
-      asm volatile("bar.sync %0, 96;" ::"r"(1u + le) : "memory");
+      // single buffer: wait until the element is out before the next round overwrites it
+      // (double buffer: the next round's barrier already orders it)
+      if constexpr (kD8VecBufs == 1) asm volatile("bar.sync %0, 96;" ::"r"(1u + le) : "memory");
     }
   }
   if (ERR) {
