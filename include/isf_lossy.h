@@ -184,14 +184,17 @@ int isf_lossy_plan_operators(const isf_lossy_plan* plan, double* F, double* B, d
                              double* w);
 /* Number of kernel launches the last compress / decompress call enqueued. */
 int isf_lossy_plan_last_launches(const isf_lossy_plan* plan);
-/* lx = 8 compress schedule.  ISF_COMPRESS_TWO_PASS (default): kept values go to
- * per-block slots and a second kernel packs them (best when few coefficients are
- * kept, the in-situ CFD case).  ISF_COMPRESS_SINGLE_PASS: the values are written to
- * their final place by the selecting kernel two rounds later, behind per-round CTA
- * aggregates (no slot round trip: best for weakly compressible data, C/F > ~0.5).
+/* lx = 8 compress schedule.  ISF_COMPRESS_TWO_PASS: kept values go to per-block slots
+ * and a second kernel packs them (best when few coefficients are kept, the in-situ CFD
+ * case).  ISF_COMPRESS_SINGLE_PASS: the values are written to their final place by the
+ * selecting kernel two rounds later, behind per-round CTA aggregates (no slot round
+ * trip: best for weakly compressible data, C/F > ~0.5).  ISF_COMPRESS_AUTO (default):
+ * single-pass when the plan's last completed compress kept more than half of the
+ * coefficients (read from host-mapped memory the kernels write: no synchronisation).
  * Streams are byte-identical either way.  Returns the previous mode, or < 0 on error. */
 #define ISF_COMPRESS_TWO_PASS 0
 #define ISF_COMPRESS_SINGLE_PASS 1
+#define ISF_COMPRESS_AUTO 2
 int isf_lossy_plan_set_compress_mode(isf_lossy_plan* plan, int mode);
 /* Device generator of the synthetic inputs: the in-situ producer
  * stand-in.  which: 0=u 1=v 2=w 3=p of the t=0 Taylor-Green vortex at GLL nodes

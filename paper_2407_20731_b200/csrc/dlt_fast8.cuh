@@ -1001,6 +1001,10 @@ __device__ void finalize_cta(const FinalizeArgs& A, double* s_red /* 4 * warps *
     }
     su[6] = total;
     su[7] = A.nblocks;
+    if (A.density) {  // zero-copy into pinned host memory: read (stale-tolerant) by the next call
+      A.density[1] = A.nblocks * 512ull;
+      A.density[0] = total;
+    }
     su[8] = A.val_off + 8 * total;
     su[9] = A.field_bytes;
     su[10] = *A.flags;

@@ -555,6 +555,7 @@ struct FinalizeArgs {
   void* stats;              // isf_lossy_stats*
   uint64_t nblocks, field_bytes, val_off;
   int with_error;
+  volatile uint64_t* density = nullptr;  // host-mapped: (kept, coefficients) of this call (lx = 8 auto schedule)
 };
 
 constexpr int kFinThreads = 512;

@@ -118,7 +118,10 @@ struct isf_lossy_plan {
   uint32_t csum_hw = 0;      // most chunks any call used (both buffers are clean beyond it)
   uint64_t* rstat = nullptr;  // single-pass compress: [round][cta] epoch-tagged aggregates
   size_t rstat_cap = 0;
-  bool use_sp = false;        // single-pass compress8 (isf_lossy_plan_set_compress_mode)
+  int c8_mode = ISF_COMPRESS_AUTO;  // lx = 8 compress schedule (isf_lossy_plan_set_compress_mode)
+  bool use_sp = false;        // the schedule of the current call
+  uint64_t* density_h = nullptr;  // pinned + mapped: (kept, coefficients) of the last lx = 8 compress
+  uint64_t* density_d = nullptr;
   int grid8dv = 0;            // decompress8 for vector fields (components = 3)
   size_t status_cap = 0;
   double* partials = nullptr;
@@ -387,9 +390,14 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, compress8_kernel<true>, kC8Warps * 32, kC8Smem));
     p->grid8c = p->sms * std::max(occ, 1);
+    // host-mapped density record of the auto schedule (zeroed: two-pass until a call completes)
+    CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&p->density_h), 2 * sizeof(uint64_t), cudaHostAllocMapped));
+    p->density_h[0] = p->density_h[1] = 0;
+    CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->density_d), p->density_h, 0));
     {
       const char* e = getenv("ISF_C8_KERNEL");  // dev override of the default schedule
-      if (e && strcmp(e, "singlepass") == 0) p->use_sp = true;
+      if (e && strcmp(e, "singlepass") == 0) p->c8_mode = ISF_COMPRESS_SINGLE_PASS;
+      if (e && strcmp(e, "twopass") == 0) p->c8_mode = ISF_COMPRESS_TWO_PASS;
     }
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress8_kernel<false>, d8_warps<false>() * 32,
                                                            d8_smem<false>()));
@@ -431,6 +439,7 @@ int isf_lossy_plan_destroy(isf_lossy_plan* p) {
   cudaFree(p->d_aux);
   cudaFree(p->crc_chunks);
   cudaFree(p->crc_n);
+  if (p->density_h) cudaFreeHost(p->density_h);
   if (p->host_stream) cudaStreamDestroy(p->host_stream);
   delete p;
   return 0;
@@ -450,10 +459,10 @@ int isf_lossy_plan_last_launches(const isf_lossy_plan* p) { return p ? p->last_l
 
 int isf_lossy_plan_set_compress_mode(isf_lossy_plan* p, int mode) {
   if (int rc = check_plan(p)) return -rc;
-  if (mode != ISF_COMPRESS_TWO_PASS && mode != ISF_COMPRESS_SINGLE_PASS)
+  if (mode != ISF_COMPRESS_TWO_PASS && mode != ISF_COMPRESS_SINGLE_PASS && mode != ISF_COMPRESS_AUTO)
     return -fail(ISF_E_INVALID_ARGUMENT, "unknown compress mode %d", mode);
-  const int prev = p->use_sp ? ISF_COMPRESS_SINGLE_PASS : ISF_COMPRESS_TWO_PASS;
-  p->use_sp = mode == ISF_COMPRESS_SINGLE_PASS;
+  const int prev = p->c8_mode;
+  p->c8_mode = mode;
   return prev;
 }
 
@@ -505,7 +514,17 @@ int isf_lossy_compress_async(isf_lossy_plan* p, const double* d_field, uint64_t 
     parts = (uint64_t)grid * kC8Warps;
     FinalizeArgs f{0, p->partials, parts, p->status, p->toff + B, ntiles, p->flags, d_stats, B,
                    B * (uint64_t)p->P * p->P * p->P * 8, hdr, 0};
+    f.density = p->density_d;
     const uint64_t cap_vals = capacity > hdr ? (capacity - hdr) / 8 : 0;
+    // schedule: auto = single-pass when the plan's last completed compress kept more than
+    // half of the coefficients (the slot round trip then moves ~2 C bytes; read without
+    // a sync from host-mapped memory the finalize writes, so it may lag a call)
+    p->use_sp = p->c8_mode == ISF_COMPRESS_SINGLE_PASS;
+    if (p->c8_mode == ISF_COMPRESS_AUTO && p->density_h) {
+      const volatile uint64_t* dh = p->density_h;
+      const uint64_t kept = dh[0], coeffs = dh[1];
+      p->use_sp = coeffs > 0 && 2 * kept > coeffs;
+    }
     if (p->use_sp) {
       const uint64_t W = (uint64_t)grid * kC8Warps;
       const uint32_t nrounds = (uint32_t)((B + W - 1) / W);

@@ -267,13 +267,14 @@ class LossyPlan:
     def last_launches(self) -> int:
         return int(self._lib.isf_lossy_plan_last_launches(self._h))
 
-    TWO_PASS, SINGLE_PASS = 0, 1
+    TWO_PASS, SINGLE_PASS, AUTO = 0, 1, 2
 
     def set_compress_mode(self, mode: int) -> int:
-        """lx = 8 compress schedule (isf_lossy_plan_set_compress_mode): TWO_PASS
-        (default; slots + packing kernel) or SINGLE_PASS (values written in place two
-        rounds after their selection; faster for weakly compressible data).  Returns
-        the previous mode; the streams are identical either way."""
+        """lx = 8 compress schedule (isf_lossy_plan_set_compress_mode): TWO_PASS (slots +
+        packing kernel), SINGLE_PASS (values written in place two rounds after their
+        selection; faster for weakly compressible data) or AUTO (default: single-pass
+        when the plan's last completed compress kept more than half of the
+        coefficients).  Returns the previous mode; the streams are identical either way."""
         rc = int(self._lib.isf_lossy_plan_set_compress_mode(self._h, int(mode)))
         if rc < 0:
             raise IsfError(ErrorCode.InvalidArgument, f"unknown compress mode {mode}")
