@@ -14,7 +14,7 @@
 #include <string>
 
 #include "../../include/isf_lossy.h"
-#include "dlt_fast8.cuh"
+#include "dlt_warp.cuh"
 #include "crc32.cuh"
 
 namespace isf {
@@ -151,6 +151,7 @@ struct isf_lossy_plan {
   uint64_t* crc_n = nullptr;
   int grid8c = 0, grid8d = 0, grid8de = 0, gridg = 0;
   size_t smem_g = 0;
+  bool use_warp = false;  // scalar lx != 8: warp-per-block decompress (dlt_warp.cuh)
 };
 
 namespace {
@@ -277,8 +278,39 @@ int launch_decompress_generic(isf_lossy_plan* p, DecompressArgs a, cudaStream_t 
   return 0;
 }
 
+template <int LX>
+int launch_decompress_w(isf_lossy_plan* p, DecompressArgs a, cudaStream_t s, uint32_t* grid_out) {
+  using G = WG<LX>;
+  const size_t sm = G::d_bytes * G::NWD;
+  static std::once_flag attr_once[64];
+  cudaError_t ae = cudaSuccess;
+  std::call_once(attr_once[p->device & 63], [&] {
+    ae = cudaFuncSetAttribute(decompress_w<LX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  });
+  CUDA_TRY(ae);
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, decompress_w<LX>, G::NWD * 32, sm));
+  occ = std::max(occ, 1);
+  const uint64_t need = (a.nblocks + G::NWD - 1) / G::NWD;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)p->sms * occ, need);
+  a.ws.total_warps = grid * G::NWD;
+  *grid_out = grid;
+  decompress_w<LX><<<grid, G::NWD * 32, sm, s>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 template <int... Ls>
 struct LxList {};
+
+template <int L0, int... Ls>
+int dispatch_decompress_w(LxList<L0, Ls...>, int lx, isf_lossy_plan* p, const DecompressArgs& a, cudaStream_t s,
+                          uint32_t* g) {
+  if (lx == L0) return launch_decompress_w<L0>(p, a, s, g);
+  if constexpr (sizeof...(Ls) > 0) return dispatch_decompress_w(LxList<Ls...>{}, lx, p, a, s, g);
+  return fail(ISF_E_INVALID_ARGUMENT, "unsupported P=%d", lx);
+}
+using WarpLx = LxList<4, 5, 6, 10, 12>;
 
 template <int L0, int... Ls>
 int dispatch_compress_generic(LxList<L0, Ls...>, int lx, isf_lossy_plan* p, const CompressArgs& a, cudaStream_t s) {
@@ -374,6 +406,12 @@ int isf_lossy_plan_create(isf_lossy_plan** out, uint32_t P, uint32_t comps, int 
   CUDA_TRY(cudaMalloc(&p->d_stats, sizeof(isf_lossy_stats)));
   CUDA_TRY(cudaMallocHost(&p->h_stats, sizeof(isf_lossy_stats)));
   build_operators((int)P, p->F, p->B, p->x, p->w);
+  {
+    const char* e = getenv("ISF_LOSSY_NO_WARP");  // dev override: decompress_generic for every lx
+    // the orders where it measured faster (profiles/r2/decompress_warp_sweep.json): lx 4 +70 %,
+    // 5 +26 %, 6 +4 %, 10 +2 %, 12 +15 %; lx 7, 9, 11 within +-4 % keep the generic kernel
+    p->use_warp = comps == 1 && (P == 4 || P == 5 || P == 6 || P == 10 || P == 12) && !(e && e[0] == '1');
+  }
   if (use_fast8(p)) {
     CUDA_TRY(cudaFuncSetAttribute(compress8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kC8Smem));
     CUDA_TRY(cudaFuncSetAttribute(decompress8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -710,7 +748,11 @@ int isf_lossy_decompress_async(isf_lossy_plan* p, const void* d_stream, uint64_t
     a.off = p->toff;
     total_ptr = p->toff + B;
     launches = 3;
-    if (int rc = dispatch_decompress_generic(AllLx{}, (int)p->P, p, a, s, &grid)) return rc;
+    if (p->use_warp && !d_original) {
+      if (int rc = dispatch_decompress_w(WarpLx{}, (int)p->P, p, a, s, &grid)) return rc;
+    } else if (int rc = dispatch_decompress_generic(AllLx{}, (int)p->P, p, a, s, &grid)) {
+      return rc;
+    }
     parts = grid;
   }
   FinalizeArgs f{1, p->partials, d_original ? parts : 0u, p->status, total_ptr, ntiles, p->flags, d_stats, B,

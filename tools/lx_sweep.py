@@ -10,8 +10,10 @@ import torch
 sys.path.insert(0, ".")
 import paper_2407_20731_b200 as PK  # noqa: E402
 
+import os
 res = {}
-for P in (6, 8, 10, 12):
+PS = [int(x) for x in os.environ.get("LXS", "6,8,10,12").split(",")]
+for P in PS:
     n = 262144
     plan = PK.LossyPlan(P, 1, 0)
     f = torch.empty(n * P ** 3, dtype=torch.float64, device="cuda")

@@ -12,7 +12,7 @@ def main(rep, kernel, so, blocks, top=40, mangled=None):
     sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                           capture_output=True, text=True).stdout
     rows = list(csv.reader(sass.splitlines()))
-    i0 = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name" and (("::" + kernel + "(") in r[1] or ("::" + kernel + "<") in r[1])][0]
+    i0 = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name" and (("::" + kernel + "(") in r[1] or ("::" + kernel + "<") in r[1] or ("::" + kernel + ">(") in r[1])][0]
     hdr = rows[i0 + 1]
     data = []
     for r in rows[i0 + 2:]:
