@@ -1270,6 +1270,9 @@ __host__ __device__ constexpr int d8_smem() { return d8_warps<ERR>() * kD8WarpBy
 #ifndef ISF_D8V_WARPS
 #define ISF_D8V_WARPS 15
 #endif
+#ifndef ISF_D8V_TMA
+#define ISF_D8V_TMA 1
+#endif
 constexpr int kD8VecWarps = ISF_D8V_WARPS;
 constexpr int kD8VecElems = kD8VecWarps / 3;
 constexpr int kD8VecBufs = kD8VecWarps <= 12 ? 2 : 1;  // element buffers per element (double buffer if it fits)
@@ -1342,6 +1345,12 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
   uint32_t ph = 0;
   // VEC: every warp runs every round (the CTA writes its 5 elements after a barrier)
   double* obuf = reinterpret_cast<double*>(smem + kNW * kD8WarpBytes);
+  __shared__ uint64_t s_ebar[VEC ? kD8VecElems : 1];  // VEC + TMA store: element buffer free
+  if constexpr (VEC) {
+    if (threadIdx.x < kD8VecElems) mbar_init(&s_ebar[threadIdx.x], 1);
+    fence_mbar_init();
+    __syncthreads();
+  }
   const uint64_t nrounds = VEC ? (B + W - 1) / W : 0;
   for (uint64_t it = 0, blk = gw; VEC ? it < nrounds : blk < B; ++it, blk += W) {
     if (!VEC || blk < B) {
@@ -1513,6 +1522,11 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
     // CTA's elements in shared memory; the error-report instantiation stores strided
     const bool vec = ERR && A.comps == 3;
     if constexpr (VEC) {
+#if ISF_D8V_TMA
+      // the element buffer's previous store has been read (one-way: the issuing thread
+      // arrived after its bulk read; a whole block of work ago, so this rarely waits)
+      if (kD8VecBufs == 1 && it > 0) mbar_wait(&s_ebar[warp / 3], (uint32_t)((it - 1) & 1));
+#endif
       // element warp / 3 of the CTA's round, component warp % 3 (the round's first block
       // is a multiple of 3: 15 blocks per CTA, 15 x grid per round)
       double* ov = obuf + ((kD8VecBufs == 2 ? (it & 1) * kD8VecElems : 0) + warp / 3) * 1536 + (warp % 3) + 3 * (2 * q + 8 * y);
@@ -1560,6 +1574,28 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
       // 128-bit stores by those 96 threads -> the buffer is free for the next round
       const uint32_t le = (uint32_t)warp / 3u;
       const uint64_t e = (blockIdx.x * (uint64_t)kNW + it * W) / 3 + le;
+#if ISF_D8V_TMA
+      // one bulk copy (TMA engine) per element: the writers' generic-proxy stores are
+      // made visible to the async proxy, then one thread of the element's first warp
+      // issues the 12 KiB store and, before the buffer is rewritten, waits for its reads
+      fence_proxy_async();
+      // double buffer: the previous round's store (its buffer is rewritten next round,
+      // after this barrier) has finished reading
+      if constexpr (kD8VecBufs == 2) {
+        if (warp % 3 == 0 && lane == 0) bulk_wait_read0();
+      }
+      asm volatile("bar.sync %0, 96;" ::"r"(1u + le) : "memory");
+      if (warp % 3 == 0 && lane == 0) {
+        if (e < B / 3) {
+          bulk_s2g(A.out + e * 1536, obuf + ((kD8VecBufs == 2 ? (it & 1) * kD8VecElems : 0) + le) * 1536, 1536 * 8);
+          bulk_commit();
+        }
+        if constexpr (kD8VecBufs == 1) {
+          bulk_wait_read0();
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_ebar[le])) : "memory");
+        }
+      }
+#else
       asm volatile("bar.sync %0, 96;" ::"r"(1u + le) : "memory");
       if (e < B / 3) {
         const double2* src = reinterpret_cast<const double2*>(
@@ -1569,9 +1605,12 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
 #pragma unroll
         for (int i = 0; i < 8; ++i) stg_stream(dst + t + 96 * i, src[t + 96 * i]);
       }
+#endif
+#if !ISF_D8V_TMA
       // single buffer: wait until the element is out before the next round overwrites it
       // (double buffer: the next round's barrier already orders it)
       if constexpr (kD8VecBufs == 1) asm volatile("bar.sync %0, 96;" ::"r"(1u + le) : "memory");
+#endif
     }
   }
   if (ERR) {
@@ -1589,6 +1628,11 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
       A.ws.partials[gw * 4 + 3] = __longlong_as_double((long long)uinf);
     }
   }
+#if ISF_D8V_TMA
+  if constexpr (VEC) {
+    if (warp % 3 == 0 && lane == 0) bulk_wait0();  // the element stores are complete
+  }
+#endif
   __shared__ double s_red[4 * kNW];
   if (last_cta(A.ws.counter + 1)) finalize_cta(P.fin, s_red);
 }
