@@ -544,6 +544,10 @@ def main():
                          "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                          "api": "isf_lossy_compress_host + isf_lossy_decompress_host (pinned host buffers; compress of field i+1 overlaps decompress of field i on a second plan)",
                          "steps": k}
+        # the bound of this leg: every step moves the fields both ways over PCIe at once
+        pb = pcie_bidir_gbs(torch, dev)
+        result["e2e"]["pcie"] = pb
+        result["e2e"]["frac_of_pcie_bound"] = result["e2e"]["value"] / world / pb["bidir_each_gbs"]
         plan2.close()
 
     if rank == 0 and not args.no_cpu and world == 1:
@@ -564,6 +568,37 @@ def main():
         dist.destroy_process_group()
     plan.close()
     return 0
+
+
+def pcie_bidir_gbs(torch, dev, nbytes=256 << 20, reps=4):
+    """Pinned host <-> device copy bandwidth on this box: each direction alone and both
+    at once (per direction).  The e2e leg moves every field H2D and back D2H with the
+    two directions overlapped, so bidir_each_gbs is its bound (field GB/s)."""
+    h1 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d1 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(up, down):
+        best = None
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            if up:
+                with torch.cuda.stream(s1):
+                    d1.copy_(h1, non_blocking=True)
+            if down:
+                with torch.cuda.stream(s2):
+                    h2.copy_(d2, non_blocking=True)
+            s1.synchronize()
+            s2.synchronize()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        return nbytes / best / 1e9
+
+    return {"h2d_gbs": timed(True, False), "d2h_gbs": timed(False, True), "bidir_each_gbs": timed(True, True),
+            "bytes": nbytes, "how": "best of 4 pinned copies of 256 MiB, wall clock around the stream syncs"}
 
 
 def cfg4_sweep(PK, torch, dev, stream, ev, hbm, n_el=262144, lxs=(6, 8, 10, 12), epss=(1e-2, 1e-5),
