@@ -321,6 +321,50 @@ def test_generic_decompress_bitexact(native, oracle, P):
         assert np.array_equal(back.values.cpu().numpy().view(np.uint64), ob.view(np.uint64)), (P, eps)
 
 
+@pytest.mark.parametrize("P", [4, 5, 6, 10, 12])
+def test_warp_decompress_shape_and_bits(native, oracle, P):
+    """The warp-per-block decode (lx 4/5/6/10/12, dlt_warp.cuh): a wrong count, a
+    truncated value region and a stray mask bit past lx^3 raise ShapeMismatch; tiny
+    (subnormal) coefficients and all-(-0) blocks reconstruct bit-identically to the
+    oracle (+0 canonicalisation)."""
+    import paper_2407_20731_b200 as PK
+    n = 27
+    u = oracle.gen_spectral(P, n)
+    f = _field(P, 1, n, u)
+    blk = PK.lossy_compress(f, PK.LossyConfig(1e-3))
+    # count of block 3 off by one
+    bad = PK.CompressedBlock(blk.stream.clone(), blk.n_elements, P, 1, blk.kept_total, blk.report)
+    c3 = int(bad.stream[12:16].cpu().numpy().view(np.uint32)[0])
+    bad.stream[12:16] = torch.from_numpy(np.array([c3 + 1], dtype=np.uint32).view(np.uint8)).cuda()
+    with pytest.raises(PK.IsfError) as ei:
+        PK.lossy_decompress(bad, f.shape)
+    assert ei.value.code == PK.ErrorCode.ShapeMismatch
+    trunc = PK.CompressedBlock(blk.stream[:-16].clone(), blk.n_elements, P, 1, blk.kept_total, blk.report)
+    with pytest.raises(PK.IsfError) as ei:
+        PK.lossy_decompress(trunc, f.shape)
+    assert ei.value.code == PK.ErrorCode.ShapeMismatch
+    N3, W = P ** 3, (P ** 3 + 63) // 64
+    if N3 % 64:
+        stray = PK.CompressedBlock(blk.stream.clone(), blk.n_elements, P, 1, blk.kept_total, blk.report)
+        mask_off = (4 * n + 15) & ~15
+        o = mask_off + 8 * (0 * W + W - 1) + 7  # last mask word of block 0, bit 63
+        stray.stream[o] = int(stray.stream[o].item()) | 0x80
+        with pytest.raises(PK.IsfError) as ei:
+            PK.lossy_decompress(stray, f.shape)
+        assert ei.value.code == PK.ErrorCode.ShapeMismatch
+    # subnormal coefficients and an all -0 block
+    v = (u * 1e-305).reshape(n, N3)
+    v[5] = -0.0
+    v = v.reshape(-1)
+    f2, blk2, ref2, _ = _compress_both(native, oracle, v, P, 1, 1e-2)
+    assert _assert_stream_parity(oracle, blk2, ref2, P, 1, 1e-2) == 0
+    back = native.lossy_decompress(blk2, f2.shape)
+    rc, ob, _ = oracle.decompress(ref2, P, 1, n)
+    assert rc == 0
+    assert np.array_equal(back.values.cpu().numpy().view(np.uint64), ob.view(np.uint64))
+    assert not np.any(back.values.cpu().numpy().view(np.uint64)[5 * N3:6 * N3])  # +0, not -0
+
+
 @pytest.mark.parametrize("case", ["tgv", "spectral_dense", "tiny_values", "signed_zeros"])
 def test_decompress_bitexact(native, oracle, case):
     """Reconstructions are bit-identical to the oracle's (incl. +0 canonicalisation,
