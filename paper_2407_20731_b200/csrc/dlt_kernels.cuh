@@ -73,6 +73,24 @@ __device__ __forceinline__ void lines2(double (&v)[N]) {
   }
 }
 
+// forward line on a strided pointer (generic kernels), returning the max |a| bits of
+// its outputs (the selection's block maximum comes out of the x sweep)
+template <int LX>
+__device__ __forceinline__ uint64_t fwd_line_ptr_mb(double* p, int stride) {
+  double v[LX];
+#pragma unroll
+  for (int i = 0; i < LX; ++i) v[i] = p[i * stride];
+  fwd_line<LX, 1, 0>(v);
+  uint64_t mb = 0;
+#pragma unroll
+  for (int i = 0; i < LX; ++i) {
+    p[i * stride] = v[i];
+    const uint64_t b = abs_bits(v[i]);
+    mb = b > mb ? b : mb;
+  }
+  return mb;
+}
+
 __device__ __forceinline__ double2 ldg_stream(const double2* p) {
   double2 r;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
@@ -89,6 +107,7 @@ __device__ __forceinline__ uint32_t claim_tile(uint32_t* counter) {
 }
 
 // --------------------------- generic (any lx, comps) ------------------------
+
 // compress_generic: one warp per block (selection is one warp's job, so wider CTAs idle;
 // 64 and 128 threads measured slower on the cfg4 sweep)
 constexpr int kGenCThreads = 32;
@@ -103,6 +122,16 @@ __host__ __device__ constexpr int gen_dthreads() {
 #endif
 }
 
+#ifndef ISF_GEN_SELECT_BIN
+#define ISF_GEN_SELECT_BIN 1
+#endif
+// orders whose compress uses select_bin (measured faster: lx 6 +12 %, 9..12 +5..17 % at
+// eps 1e-2 / 1e-5; lx 4, 5, 7 up to 7 % slower with dense spectra); its 21-bit bin
+// planes are exact for lx^3 <= 2048 candidates
+__host__ __device__ constexpr bool gen_select_bin(int lx) {
+  return ISF_GEN_SELECT_BIN && (lx == 6 || (lx >= 9 && lx <= 12));
+}
+
 template <int LX>
 struct GenSmem {
   static constexpr int N3 = LX * LX * LX;
@@ -110,7 +139,10 @@ struct GenSmem {
   static constexpr size_t u_off = 0;
   static constexpr size_t idx_off = u_off + sizeof(double) * N3;
   static constexpr size_t hist_off = ((idx_off + sizeof(uint16_t) * N3) + 15) & ~size_t(15);
-  static constexpr size_t mask_off = hist_off + 64 * 8;
+  // selection scratch: the binned cut search (3 x 256 u32 bins, 32 candidate keys and
+  // indices); the radix fallback reuses its first 512 B as 64 u64 bins
+  static constexpr size_t hist_bytes = gen_select_bin(LX) ? 3 * 256 * 4 + 32 * 8 + 32 * 4 : 64 * 8;
+  static constexpr size_t mask_off = hist_off + hist_bytes;
   static constexpr size_t misc_off = mask_off + 64 * 8;
   static constexpr size_t bytes = misc_off + 64;
 };
@@ -236,6 +268,254 @@ __device__ void select_generic(double* u, uint64_t eps_m, int eps_e, uint16_t* c
   __syncwarp();
 }
 
+// radix-select source with the tiny-block pre-scale applied on the fly (select_bin's
+// fallback; keys of the pre-scaled coefficients, as select_generic)
+struct SrcIndirectPre {
+  static constexpr bool kCompact = true;
+  const double* a;
+  uint16_t* idxs;
+  double pre;
+  __device__ __forceinline__ void operator()(int p, uint64_t& k, uint32_t& ix) const {
+    ix = idxs[p];
+    k = abs_bits(__dmul_rn(a[ix], pre));
+  }
+  __device__ __forceinline__ void set(int p, uint32_t ix) const { idxs[p] = (uint16_t)ix; }
+};
+
+// Truncation rule v2 on warp 0 over the block's coefficients u[] (natural order), the
+// same result as select_generic with fewer passes: the block maximum mb comes from the
+// x sweep, the 2^k scale is folded into the energy constants (RD((a 2^k)^2) == RD(a^2)
+// 2^2k while a^2 is normal; below, both floors are 0), and when the sure-kept set does
+// not settle the block the cut is found by a binned search over the compacted
+// candidates only (256 eighth-binades of |a| below the maximum, exact 21-bit-plane u32
+// shared atomics, then a warp bitonic sort of the <= 32 cut-bin candidates), with the
+// radix select as the fallback for crowded bins and tiny blocks.  Kept bits are OR-ed
+// into mw[] (one u32 per 32 coefficients, zero on entry).  mb > 0, finite.
+template <int LX>
+__device__ __noinline__ void select_bin(const double* u, uint64_t mb, uint64_t eps_m, int eps_e, uint16_t* cidx,
+                                        uint32_t* bins, uint64_t* ckey, uint32_t* cix, uint32_t* mw, uint64_t& T_out,
+                                        uint64_t& hd_out, int& eT_out, int& eD_out) {
+  constexpr int N3 = LX * LX * LX, NR = (N3 + 31) / 32;
+  constexpr uint64_t C52 = 0x4330000000000000ull;
+  const LaneGroup<32> g;
+  const int lane = g.rank;
+  const uint32_t lt = (1u << lane) - 1u;
+  constexpr int EM = energy_EM(LX), HM = EM / 2;
+  int s;
+  {
+    const uint32_t hm = (uint32_t)(mb >> 32);
+    s = hm >= 0x00100000u ? (int)(hm >> 20) - 1022 : 64 - __clzll((long long)mb) - 1074;
+  }
+  int k = HM - s;
+  const int k0 = k;
+  const bool tiny = k > 1023;
+  const double pre = tiny ? pow2d(k - 1023) : 1.0;
+  if (tiny) k = 1023;
+  const double f = pow2d(k);
+  int h;
+  {
+    const double xm = __dmul_rn(__longlong_as_double((long long)mb), pre);
+    const double xs = __dmul_rn(xm, f);
+    h = (EM - 2 * HM) + (__dmul_rd(xs, xs) < pow2d(2 * HM - 1) ? 1 : 0);
+  }
+  const double sA = pow2d(h);
+  const bool fold = !tiny && 2 * k + h <= 1000;
+  uint64_t tl = 0;
+  if (fold) {
+    const double fA = pow2d(2 * k + h);
+#pragma unroll 4
+    for (int p = lane; p < N3; p += 32) {
+      const double a = u[p];
+      tl += (uint64_t)__double_as_longlong(__fma_rd(__dmul_rd(a, a), fA, kTwo52)) - C52;
+    }
+  } else {
+#pragma unroll 4
+    for (int p = lane; p < N3; p += 32) {
+      const double x = __dmul_rn(__dmul_rn(u[p], pre), f);
+      tl += (uint64_t)__double_as_longlong(__fma_rd(__dmul_rd(x, x), sA, kTwo52)) - C52;
+    }
+  }
+  const uint64_t T = g.sum(tl);
+  T_out = T;
+  int Gs;
+  const uint64_t thr = thr_v2(T, eps_m, eps_e, h, Gs);
+  const double sB = pow2d(h + Gs);
+  eT_out = -2 * k0 - h;
+  eD_out = -2 * k0 - h - Gs;
+  const bool foldB = fold && 2 * k + h + Gs <= 1000;
+  const double fB = foldB ? pow2d(2 * k + h + Gs) : 1.0;
+  // scale B: t = 2^52 + floor(e 2^(h+G)) (>= 2^53: saturated, always kept)
+  auto tB = [&](double a) -> double {
+    if (foldB) return __fma_rd(__dmul_rd(a, a), fB, kTwo52);
+    const double x = __dmul_rn(__dmul_rn(a, pre), f);
+    return __fma_rd(__dmul_rd(x, x), sB, kTwo52);
+  };
+  const double tthr = __longlong_as_double((long long)(C52 + thr));  // hi > thr  <=>  t >= tthr
+  const uint64_t thrn = thr / (uint64_t)N3;
+  uint64_t SN = 0, SL = 0;
+  uint32_t nc = 0;
+  for (int rr = 0; rr < NR; ++rr) {
+    const int p = 32 * rr + lane;
+    bool sure = false, cand = false;
+    if (p < N3) {
+      const double t = tB(u[p]);
+      if (t >= tthr) {
+        sure = true;
+      } else {
+        const uint64_t hv = (uint64_t)__double_as_longlong(t) - C52 + 1ull;
+        SN += hv;
+        if (hv <= thrn) SL += hv; else cand = true;
+      }
+    }
+    const uint32_t bk = __ballot_sync(0xffffffffu, sure);
+    const uint32_t bc = __ballot_sync(0xffffffffu, cand);
+    if (lane == 0) mw[rr] = bk;
+    if (cand) cidx[nc + __popc(bc & lt)] = (uint16_t)p;
+    nc += __popc(bc);
+  }
+  SN = g.sum(SN);
+  if (SN <= thr) {
+    hd_out = SN;
+    __syncwarp();
+    return;
+  }
+  SL = g.sum(SL);
+  const uint64_t R = thr - SL;
+  const int bbase = (int)(mb >> 49) - 255;
+  if (!tiny) {
+#pragma unroll
+    for (int j = 0; j < 3 * 256 / 32; ++j) bins[lane + 32 * j] = 0u;
+    __syncwarp();
+    for (int c = lane; c < (int)nc; c += 32) {
+      const double a = u[cidx[c]];
+      const uint64_t kk = abs_bits(a);
+      const uint64_t hv = (uint64_t)__double_as_longlong(tB(a)) - C52 + 1ull;
+      const int bn = ::max((int)(kk >> 49) - bbase, 0);
+      atomicAdd(&bins[bn], (uint32_t)(hv & 0x1FFFFFu));
+      atomicAdd(&bins[256 + bn], (uint32_t)((hv >> 21) & 0x1FFFFFu));
+      atomicAdd(&bins[512 + bn], (uint32_t)(hv >> 42));
+    }
+    __syncwarp();
+    uint64_t bs[8];
+    uint64_t lsum = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int b = 8 * lane + q;
+      bs[q] = (uint64_t)bins[b] + ((uint64_t)bins[256 + b] << 21) + ((uint64_t)bins[512 + b] << 42);
+      lsum += bs[q];
+    }
+    uint64_t x = lsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    const uint64_t run = x - lsum;
+    uint32_t dloc = 256;
+    uint64_t exloc = 0;
+#pragma unroll
+    for (int q = 7; q >= 0; --q) {
+      uint64_t pq = run;
+#pragma unroll
+      for (int w2 = 0; w2 < q; ++w2) pq += bs[w2];
+      if (pq + bs[q] > R) { dloc = 8 * lane + q; exloc = pq; }
+    }
+    const uint32_t d = g.min(dloc);
+    if (d < 256) {
+      const uint64_t ex = __shfl_sync(0xffffffffu, exloc, (int)(d >> 3));
+      uint32_t ncd = 0;  // the cut bin's candidates (key, index)
+      for (int c0 = 0; c0 < (int)nc; c0 += 32) {
+        const int c = c0 + lane;
+        uint64_t kk = 0;
+        uint32_t ix = 0;
+        bool in = false;
+        if (c < (int)nc) {
+          ix = cidx[c];
+          kk = abs_bits(u[ix]);
+          in = ::max((int)(kk >> 49) - bbase, 0) == (int)d;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, in);
+        const uint32_t pos = ncd + __popc(bal & lt);
+        if (in && pos < 32) { ckey[pos] = kk; cix[pos] = ix; }
+        ncd += __popc(bal);
+      }
+      __syncwarp();
+      if (ncd <= 32) {
+        uint64_t key = lane < (int)ncd ? ckey[lane] : ~0ull;
+        uint32_t kix = lane < (int)ncd ? cix[lane] : 0xffffffffu;
+#pragma unroll
+        for (int kb = 2; kb <= 32; kb <<= 1)  // bitonic sort by key (the index rides along)
+#pragma unroll
+          for (int j = kb >> 1; j > 0; j >>= 1) {
+            const uint64_t o = __shfl_xor_sync(0xffffffffu, key, j);
+            const uint32_t oi = __shfl_xor_sync(0xffffffffu, kix, j);
+            const bool up = ((lane & kb) == 0), lower = ((lane & j) == 0);
+            const bool sw = (lower == up) ? (o < key) : (o > key);
+            if (sw) { key = o; kix = oi; }
+          }
+        const bool live = lane < (int)ncd;
+        const uint64_t hv =
+            live ? (uint64_t)__double_as_longlong(tB(__longlong_as_double((long long)key))) - C52 + 1ull : 0ull;
+        uint64_t cs = hv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint64_t t = __shfl_up_sync(0xffffffffu, cs, o);
+          if (lane >= o) cs += t;
+        }
+        const uint32_t over = __ballot_sync(0xffffffffu, live && cs > R - ex);
+        if (over) {
+          const int ic = __ffs(over) - 1;
+          const uint64_t K = __shfl_sync(0xffffffffu, key, ic);
+          const uint64_t dis = __shfl_sync(0xffffffffu, cs - hv, ic);
+          const bool tied = live && key == K;
+          const uint32_t tiedbefore = __popc(__ballot_sync(0xffffffffu, tied && lane < ic));
+          uint32_t icut = 0xffffffffu;
+          if (tiedbefore) {
+            // keep the (gcount - tiedbefore) smallest indices among the tied (SPEC.md:225
+            // stable order): icut = the tied index of that rank
+            const uint32_t gcount = __popc(__ballot_sync(0xffffffffu, tied));
+            const uint32_t want = gcount - tiedbefore;
+            uint32_t rank = 0;
+#pragma unroll 1
+            for (int j = 0; j < 32; ++j) {
+              const uint32_t oj = __shfl_sync(0xffffffffu, kix, j);
+              const uint64_t kj = __shfl_sync(0xffffffffu, key, j);
+              rank += (j < (int)ncd && kj == K && oj < kix) ? 1u : 0u;
+            }
+            icut = g.min((tied && rank == want) ? kix : 0xffffffffu);
+          }
+          hd_out = SL + ex + dis;
+          for (int c = lane; c < (int)nc; c += 32) {
+            const uint32_t ix = cidx[c];
+            const uint64_t kk = abs_bits(u[ix]);
+            if (kk > K || (kk == K && ix < icut)) atomicOr(&mw[ix >> 5], 1u << (ix & 31));
+          }
+          __syncwarp();
+          return;
+        }
+      }
+    }
+  }
+  // crowded cut bin / tiny block: the radix select over the candidates (exact, any case)
+  __syncwarp();
+  uint64_t tstar, dsum;
+  uint32_t icut;
+  radix_select<32>(g, SrcIndirectPre{u, cidx, pre}, (int)nc, R, f, sB, reinterpret_cast<unsigned long long*>(bins),
+                   tstar, icut, dsum);
+  for (int rr = 0; rr < NR; ++rr) {
+    const int p = 32 * rr + lane;
+    bool kept = false;
+    if (p < N3) {
+      const uint64_t kk = abs_bits(__dmul_rn(u[p], pre));
+      kept = kk > tstar || (kk == tstar && (uint32_t)p < icut);
+    }
+    const uint32_t b = __ballot_sync(0xffffffffu, kept);
+    if (lane == 0) mw[rr] = b;
+  }
+  hd_out = SL + dsum;
+  __syncwarp();
+}
+
 // RelativeLInf selection on warp 0 (dlt_common.cuh radix_select_w)
 template <int LX>
 __device__ void select_linf(const double* u, double umax, double eps, unsigned long long* hist, uint64_t* maskw,
@@ -343,7 +623,11 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
     __syncthreads();
     for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + (l / N) * N2 + (l % N), N);  // y
     __syncthreads();
-    for (int l = tid; l < N2; l += kGenCThreads) fwd_line_ptr<LX>(u + l * N, 1);                     // x
+    uint64_t mbl = 0;  // the block maximum, from the x sweep's outputs
+    for (int l = tid; l < N2; l += kGenCThreads) {
+      const uint64_t m = fwd_line_ptr_mb<LX>(u + l * N, 1);  // x
+      mbl = m > mbl ? m : mbl;
+    }
     __syncthreads();
     if (kGenCThreads == 32 || warp == 0) {  // single-warp CTA: no divergent region
       uint64_t T, hd;
@@ -354,7 +638,22 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
         T = hd = 0;
         eT = eD = 0;
       } else {
+        if constexpr (gen_select_bin(LX)) {
+        const uint64_t mb = LaneGroup<32>().max(mbl);
+        for (int w = lane; w < 64; w += 32) maskw[w] = 0ull;
+        T = hd = 0;
+        eT = eD = 0;
+        nf = mb >= 0x7ff0000000000000ull;
+        __syncwarp();
+        if (!nf && mb != 0)
+          select_bin<LX>(u, mb, A.eps_m, A.eps_e, cidx, reinterpret_cast<uint32_t*>(hist),
+                         reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(hist) + 3 * 256 * 4),
+                         reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(hist) + 3 * 256 * 4 + 32 * 8),
+                         reinterpret_cast<uint32_t*>(maskw), T, hd, eT, eD);
+        } else {
+        (void)mbl;
         select_generic<LX>(u, A.eps_m, A.eps_e, cidx, hist, maskw, T, hd, eT, eD, nf);
+        }
       }
       if (nf) {
         for (int w = lane; w < W; w += 32) maskw[w] = 0ull;
