@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
     if (LX <= 10 && A.comps == 1 && !A.norm) {
 #pragma unroll 4
       for (int p = tid; p < N3; p += kGenCThreads) u[p] = src[p];
-    } else {
+    } else {  // (also for RelativeL2 at lx > 10: a loop without the maximum measured 8-10 % slower)
       for (int p = tid; p < N3; p += kGenCThreads) {
         const double x = src[(uint64_t)p * A.comps];
         u[p] = x;
@@ -677,8 +677,13 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
     }
     __syncthreads();
     double* slot = A.vslot + blk * (uint64_t)N3;
-    for (int p = tid; p < N3; p += kGenCThreads)
-      if ((maskw[p >> 6] >> (p & 63)) & 1ull) slot[p] = u[p];
+    static_assert(kGenCThreads == 32, "one 32-bit mask half per round");
+    const uint32_t* mw32 = reinterpret_cast<const uint32_t*>(maskw);
+    for (int r = 0; 32 * r < N3; ++r) {
+      const uint32_t m = mw32[r];
+      if (m == 0u) continue;  // warp-uniform: the round keeps nothing
+      if ((m >> tid) & 1u) slot[32 * r + tid] = u[32 * r + tid];
+    }
     next = __shfl_sync(0xffffffffu, next, 0);
   }
 }
