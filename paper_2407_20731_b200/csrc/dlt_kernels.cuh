@@ -128,6 +128,11 @@ __host__ __device__ constexpr int gen_dthreads() {
 // orders whose compress uses select_bin (measured faster: lx 6 +12 %, 9..12 +5..17 % at
 // eps 1e-2 / 1e-5; lx 4, 5, 7 up to 7 % slower with dense spectra); its 21-bit bin
 // planes are exact for lx^3 <= 2048 candidates
+// select_bin's bins below the block maximum: 128 quarter binades of |a| up to lx 10
+// (less to clear and scan: +2.5..8 %), 256 eighth binades at lx 11 / 12 (quarter
+// binades crowd the cut bin past 32 candidates at eps 1e-5 there: -18 / -30 %)
+__host__ __device__ constexpr int gen_bins(int lx) { return lx >= 11 ? 256 : 128; }
+__host__ __device__ constexpr int gen_bin_shift(int lx) { return gen_bins(lx) == 256 ? 49 : 50; }
 __host__ __device__ constexpr bool gen_select_bin(int lx) {
   return ISF_GEN_SELECT_BIN && (lx == 6 || (lx >= 9 && lx <= 12));
 }
@@ -139,9 +144,9 @@ struct GenSmem {
   static constexpr size_t u_off = 0;
   static constexpr size_t idx_off = u_off + sizeof(double) * N3;
   static constexpr size_t hist_off = ((idx_off + sizeof(uint16_t) * N3) + 15) & ~size_t(15);
-  // selection scratch: the binned cut search (3 x 256 u32 bins, 32 candidate keys and
-  // indices); the radix fallback reuses its first 512 B as 64 u64 bins
-  static constexpr size_t hist_bytes = gen_select_bin(LX) ? 3 * 256 * 4 + 32 * 8 + 32 * 4 : 64 * 8;
+  // selection scratch: the binned cut search (3 x gen_bins u32 bins; the 32 cut-bin keys and
+  // indices reuse them once read); the radix fallback reuses the first 512 B as 64 u64 bins
+  static constexpr size_t hist_bytes = gen_select_bin(LX) ? (3 * gen_bins(LX) * 4 > 512 ? 3 * gen_bins(LX) * 4 : 512) : 64 * 8;
   static constexpr size_t mask_off = hist_off + hist_bytes;
   static constexpr size_t misc_off = mask_off + 64 * 8;
   static constexpr size_t bytes = misc_off + 64;
@@ -287,7 +292,7 @@ struct SrcIndirectPre {
 // x sweep, the 2^k scale is folded into the energy constants (RD((a 2^k)^2) == RD(a^2)
 // 2^2k while a^2 is normal; below, both floors are 0), and when the sure-kept set does
 // not settle the block the cut is found by a binned search over the compacted
-// candidates only (256 eighth-binades of |a| below the maximum, exact 21-bit-plane u32
+// candidates only (gen_bins quarter / eighth binades of |a| below the maximum, exact 21-bit-plane u32
 // shared atomics, then a warp bitonic sort of the <= 32 cut-bin candidates), with the
 // radix select as the fallback for crowded bins and tiny blocks.  Kept bits are OR-ed
 // into mw[] (one u32 per 32 coefficients, zero on entry).  mb > 0, finite.
@@ -381,29 +386,31 @@ __device__ __noinline__ void select_bin(const double* u, uint64_t mb, uint64_t e
   }
   SL = g.sum(SL);
   const uint64_t R = thr - SL;
-  const int bbase = (int)(mb >> 49) - 255;
+  constexpr int NB = gen_bins(LX), BPL = NB / 32, SH = gen_bin_shift(LX);
+  const int bbase = (int)(mb >> SH) - (NB - 1);
   if (!tiny) {
 #pragma unroll
-    for (int j = 0; j < 3 * 256 / 32; ++j) bins[lane + 32 * j] = 0u;
+    for (int j = 0; j < 3 * NB / 32; ++j) bins[lane + 32 * j] = 0u;
     __syncwarp();
     for (int c = lane; c < (int)nc; c += 32) {
       const double a = u[cidx[c]];
       const uint64_t kk = abs_bits(a);
       const uint64_t hv = (uint64_t)__double_as_longlong(tB(a)) - C52 + 1ull;
-      const int bn = ::max((int)(kk >> 49) - bbase, 0);
+      const int bn = ::max((int)(kk >> SH) - bbase, 0);
       atomicAdd(&bins[bn], (uint32_t)(hv & 0x1FFFFFu));
-      atomicAdd(&bins[256 + bn], (uint32_t)((hv >> 21) & 0x1FFFFFu));
-      atomicAdd(&bins[512 + bn], (uint32_t)(hv >> 42));
+      atomicAdd(&bins[NB + bn], (uint32_t)((hv >> 21) & 0x1FFFFFu));
+      atomicAdd(&bins[2 * NB + bn], (uint32_t)(hv >> 42));
     }
     __syncwarp();
-    uint64_t bs[8];
+    uint64_t bs[BPL];
     uint64_t lsum = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int b = 8 * lane + q;
-      bs[q] = (uint64_t)bins[b] + ((uint64_t)bins[256 + b] << 21) + ((uint64_t)bins[512 + b] << 42);
+    for (int q = 0; q < BPL; ++q) {
+      const int b = BPL * lane + q;
+      bs[q] = (uint64_t)bins[b] + ((uint64_t)bins[NB + b] << 21) + ((uint64_t)bins[2 * NB + b] << 42);
       lsum += bs[q];
     }
+    __syncwarp();  // bins are read: the cut-bin candidates below reuse their storage
     uint64_t x = lsum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -411,18 +418,18 @@ __device__ __noinline__ void select_bin(const double* u, uint64_t mb, uint64_t e
       if (lane >= o) x += t;
     }
     const uint64_t run = x - lsum;
-    uint32_t dloc = 256;
+    uint32_t dloc = NB;
     uint64_t exloc = 0;
 #pragma unroll
-    for (int q = 7; q >= 0; --q) {
+    for (int q = BPL - 1; q >= 0; --q) {
       uint64_t pq = run;
 #pragma unroll
       for (int w2 = 0; w2 < q; ++w2) pq += bs[w2];
-      if (pq + bs[q] > R) { dloc = 8 * lane + q; exloc = pq; }
+      if (pq + bs[q] > R) { dloc = BPL * lane + q; exloc = pq; }
     }
     const uint32_t d = g.min(dloc);
-    if (d < 256) {
-      const uint64_t ex = __shfl_sync(0xffffffffu, exloc, (int)(d >> 3));
+    if (d < (uint32_t)NB) {
+      const uint64_t ex = __shfl_sync(0xffffffffu, exloc, (int)(d / BPL));
       uint32_t ncd = 0;  // the cut bin's candidates (key, index)
       for (int c0 = 0; c0 < (int)nc; c0 += 32) {
         const int c = c0 + lane;
@@ -432,7 +439,7 @@ __device__ __noinline__ void select_bin(const double* u, uint64_t mb, uint64_t e
         if (c < (int)nc) {
           ix = cidx[c];
           kk = abs_bits(u[ix]);
-          in = ::max((int)(kk >> 49) - bbase, 0) == (int)d;
+          in = ::max((int)(kk >> SH) - bbase, 0) == (int)d;
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, in);
         const uint32_t pos = ncd + __popc(bal & lt);
@@ -647,8 +654,8 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
         __syncwarp();
         if (!nf && mb != 0)
           select_bin<LX>(u, mb, A.eps_m, A.eps_e, cidx, reinterpret_cast<uint32_t*>(hist),
-                         reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(hist) + 3 * 256 * 4),
-                         reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(hist) + 3 * 256 * 4 + 32 * 8),
+                         reinterpret_cast<uint64_t*>(hist),  // cut-bin keys / indices: in the read bins
+                         reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(hist) + 32 * 8),
                          reinterpret_cast<uint32_t*>(maskw), T, hd, eT, eD);
         } else {
         (void)mbl;
