@@ -125,17 +125,17 @@ __host__ __device__ constexpr int gen_dthreads() {
 #ifndef ISF_GEN_SELECT_BIN
 #define ISF_GEN_SELECT_BIN 1
 #endif
-// orders whose compress uses select_bin (measured faster: lx 6 +12 %, 9..12 +5..17 % at
-// eps 1e-2 / 1e-5; lx 4, 5, 7 up to 7 % slower with dense spectra); its 21-bit bin
-// planes are exact for lx^3 <= 2048 candidates
+// orders whose compress uses select_bin (measured against select_generic on the cfg4
+// spectra, eps 1e-2 / 1e-5: lx 4 +10 / -4 %, 5 +20 / +1 %, 6 +7..12 %, 7 +10 / +3 %,
+// 9..12 +5..17 %; lx 3 -6 %); its 21-bit bin planes are exact for lx^3 <= 2048 candidates
+__host__ __device__ constexpr bool gen_select_bin(int lx) {
+  return ISF_GEN_SELECT_BIN && lx >= 4 && lx <= 12;
+}
 // select_bin's bins below the block maximum: 128 quarter binades of |a| up to lx 10
 // (less to clear and scan: +2.5..8 %), 256 eighth binades at lx 11 / 12 (quarter
 // binades crowd the cut bin past 32 candidates at eps 1e-5 there: -18 / -30 %)
 __host__ __device__ constexpr int gen_bins(int lx) { return lx >= 11 ? 256 : 128; }
 __host__ __device__ constexpr int gen_bin_shift(int lx) { return gen_bins(lx) == 256 ? 49 : 50; }
-__host__ __device__ constexpr bool gen_select_bin(int lx) {
-  return ISF_GEN_SELECT_BIN && (lx == 6 || (lx >= 9 && lx <= 12));
-}
 
 template <int LX>
 struct GenSmem {
