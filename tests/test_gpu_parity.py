@@ -365,7 +365,7 @@ def test_warp_decompress_shape_and_bits(native, oracle, P):
     assert not np.any(back.values.cpu().numpy().view(np.uint64)[5 * N3:6 * N3])  # +0, not -0
 
 
-@pytest.mark.parametrize("case", ["tgv", "spectral_dense", "tiny_values", "signed_zeros"])
+@pytest.mark.parametrize("case", ["tgv", "spectral_dense", "tiny_values", "signed_zeros", "mixed"])
 def test_decompress_bitexact(native, oracle, case):
     """Reconstructions are bit-identical to the oracle's (incl. +0 canonicalisation,
     DESIGN.md 3.3), also for streams whose values are subnormal, zero or -0 and
@@ -376,6 +376,11 @@ def test_decompress_bitexact(native, oracle, case):
     if case == "tgv":
         u = oracle.gen_tgv(E, P, 3)
         eps = 1e-3
+    elif case == "mixed":  # sparse TGV blocks interleaved with dense spectral ones
+        t = oracle.gen_tgv(E, P, 0).reshape(n_el, P ** 3)
+        sp = oracle.gen_spectral(P, n_el).reshape(n_el, P ** 3)
+        u = np.where((np.arange(n_el) % 3 == 1)[:, None], sp, t).reshape(-1).copy()
+        eps = 1e-5
     else:
         u = oracle.gen_spectral(P, n_el)
         eps = 1e-2 if case != "spectral_dense" else 1e-6
