@@ -1094,19 +1094,62 @@ __global__ void __launch_bounds__(kOffThreads) block_offsets8_kernel(const uint8
 // accumulated in csum (no look-back chain), the in-chunk offsets a block scan.  CTA
 // nchunks clears the other csum buffer (used by the next call) and reduces the
 // statistics, concurrently with the copies.
-constexpr int kCompactThreads = 1024;
-static_assert(kCompactThreads == kOffChunk, "one thread per block of a chunk");
+// Compress epilogue: one CTA per 1024-block chunk, 512 threads, two blocks per thread
+// (64 registers: every mask word and value load of a sparse block in flight at once;
+// the 1024-thread / 32-register version walked the mask words in dependent rounds).
+constexpr int kCompactThreads = 512;
+static_assert(2 * kCompactThreads == kOffChunk, "two blocks of a chunk per thread");
+
+// up to 16 kept values of a sparse block (slot in natural index order): all mask words,
+// then all loads, then all stores
+__device__ __forceinline__ void sparse_copy16(const double* src, const uint4* m4, double* dst, uint32_t c) {
+  uint64_t mw[8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 t = m4[q];  // plain load: the masks stay in L2 for the decompress that follows
+    mw[2 * q] = ((uint64_t)t.y << 32) | t.x;
+    mw[2 * q + 1] = ((uint64_t)t.w << 32) | t.z;
+  }
+  uint32_t nz = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) nz |= (mw[w] ? 1u : 0u) << w;
+  uint64_t mm = 0;
+  int wb = 0;
+  double v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    v[k] = 0.0;
+    if ((uint32_t)k < c) {
+      if (mm == 0) {  // next non-empty word (a select chain: no dynamic register index)
+        const int w = __ffs(nz) - 1;
+        nz &= nz - 1;
+        uint64_t t = mw[0];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) t = w == q ? mw[q] : t;
+        mm = t;
+        wb = 64 * w;
+      }
+      const int j = wb + __ffsll((long long)mm) - 1;
+      mm &= mm - 1;
+      v[k] = __ldcs(src + j);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    if ((uint32_t)k < c) dst[k] = v[k];
+}
 
 __global__ void __launch_bounds__(kCompactThreads, 2) compact8_kernel(uint8_t* stream, uint64_t nblocks, uint64_t mask_off,
                                                                   const uint64_t* csum, uint64_t* csum_next,
                                                                   const double* vslot, double* vals,
                                                                   uint64_t cap_vals, uint64_t* total_out,
                                                                   uint32_t nclear, FinalizeArgs fin) {
-  __shared__ uint64_t s_w[kCompactThreads / 32];
+  constexpr int NW = kCompactThreads / 32;
+  __shared__ uint64_t s_w[2 * NW];
   __shared__ uint64_t s_prefix;
-  __shared__ double s_red[4 * (kCompactThreads / 32)];
-  __shared__ uint64_t s_off[kCompactThreads];  // dense list: value offsets
-  __shared__ uint16_t s_dense[kCompactThreads];
+  __shared__ double s_red[4 * NW];
+  __shared__ uint64_t s_off[2 * kCompactThreads];  // dense list: value offsets
+  __shared__ uint16_t s_dense[2 * kCompactThreads];
   __shared__ uint32_t s_ndense;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nchunks = (uint32_t)((nblocks + kOffChunk - 1) / kOffChunk);
@@ -1123,9 +1166,11 @@ __global__ void __launch_bounds__(kCompactThreads, 2) compact8_kernel(uint8_t* s
     __syncthreads();
     if (tid == 0) {
       uint64_t t = 0;
-      for (int w = 0; w < kCompactThreads / 32; ++w) t += s_w[w];
+      for (int w = 0; w < NW; ++w) t += s_w[w];
       *total_out = t;
       if (t > cap_vals) atomicOr(fin.flags, kFlagOverflow);
+      uint32_t* counts = reinterpret_cast<uint32_t*>(stream);
+      for (uint64_t pb = nblocks; pb < ((nblocks + 3) & ~3ull); ++pb) counts[pb] = 0;  // 16-B pad
       __threadfence_block();
     }
     __syncthreads();
@@ -1138,85 +1183,72 @@ __global__ void __launch_bounds__(kCompactThreads, 2) compact8_kernel(uint8_t* s
     for (uint32_t c = lane; c < chunk; c += 32) a += csum[c];
 #pragma unroll
     for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if (lane == 0) s_prefix = a;
+    if (lane == 0) {
+      s_prefix = a;
+      s_ndense = 0;
+    }
   }
-  uint32_t* counts = reinterpret_cast<uint32_t*>(stream);
+  const uint32_t* counts = reinterpret_cast<const uint32_t*>(stream);
   const uint16_t* masks16 = reinterpret_cast<const uint16_t*>(stream + mask_off);  // 32 words per block
-  const uint64_t b = (uint64_t)chunk * kOffChunk + tid;
-  const uint32_t c = b < nblocks ? counts[b] : 0u;
-  uint32_t x = c;
+  const uint64_t b0 = (uint64_t)chunk * kOffChunk + tid, b1 = b0 + kCompactThreads;
+  const uint32_t c0 = b0 < nblocks ? counts[b0] : 0u, c1 = b1 < nblocks ? counts[b1] : 0u;
+  uint32_t x0 = c0, x1 = c1;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += t;
-  }
-  if (lane == 31) s_w[warp] = x;
-  __syncthreads();
-  uint64_t wex = 0;
-  for (int w = 0; w < warp; ++w) wex += s_w[w];
-  const uint64_t e = s_prefix + wex + x - c;  // the block's first value
-  if (b + 1 == nblocks)  // zero the 16-B pad of the counts
-    for (uint64_t pb = nblocks; pb < ((nblocks + 3) & ~3ull); ++pb) counts[pb] = 0;
-  if (tid == 0) s_ndense = 0;
-  __syncthreads();
-  // Sparse blocks (<= 16 kept, slot in natural index order): one thread walks the
-  // block's mask.  Dense blocks (slot layout [r][lane]) go to a list that whole warps
-  // pack below (thread-serial copies of hundreds of values would dominate).
-  if (c > 16) {
-    if (e + c <= cap_vals) {
-      const uint32_t k = atomicAdd(&s_ndense, 1u);
-      s_dense[k] = (uint32_t)tid;
-      s_off[k] = e;
-    }
-  } else if (c && e + c <= cap_vals) {
-    const double* src = vslot + b * 512;
-    const ulonglong2* mk = reinterpret_cast<const ulonglong2*>(masks16 + b * 32);
-    double* dst = vals + e;
-#pragma unroll
-    for (int w2 = 0; w2 < 4; ++w2) {
-      const ulonglong2 q2 = mk[w2];
-#pragma unroll
-      for (int hw = 0; hw < 2; ++hw) {
-        uint64_t mm = hw ? q2.y : q2.x;
-        const int w = 2 * w2 + hw;
-        while (mm) {  // up to four set bits per round, their loads in flight together
-          int j[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            j[q] = mm ? 64 * w + (__ffsll((long long)mm) - 1) : -1;
-            mm &= mm - 1;
-          }
-          double t4[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) t4[q] = j[q] >= 0 ? __ldcs(src + j[q]) : 0.0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (j[q] >= 0) *dst++ = t4[q];
-        }
-      }
+    const uint32_t t0 = __shfl_up_sync(0xffffffffu, x0, o), t1 = __shfl_up_sync(0xffffffffu, x1, o);
+    if (lane >= o) {
+      x0 += t0;
+      x1 += t1;
     }
   }
+  if (lane == 31) {
+    s_w[warp] = x0;
+    s_w[NW + warp] = x1;
+  }
+  __syncthreads();
+  uint64_t w0 = 0, w1 = 0, t0 = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    w0 += w < warp ? s_w[w] : 0ull;
+    w1 += w < warp ? s_w[NW + w] : 0ull;
+    t0 += s_w[w];
+  }
+  const uint64_t e0 = s_prefix + w0 + x0 - c0, e1 = s_prefix + t0 + w1 + x1 - c1;  // the blocks' first values
+  // Sparse blocks (<= 16 kept, slot in natural index order) are copied by their thread.
+  // Dense blocks (slot layout [r][lane]) go to a list that whole warps pack below
+  // (thread-serial copies of hundreds of values would dominate).
+  if (c0 > 16 && e0 + c0 <= cap_vals) {
+    const uint32_t k = atomicAdd(&s_ndense, 1u);
+    s_dense[k] = (uint16_t)tid;
+    s_off[k] = e0;
+  }
+  if (c1 > 16 && e1 + c1 <= cap_vals) {
+    const uint32_t k = atomicAdd(&s_ndense, 1u);
+    s_dense[k] = (uint16_t)(tid + kCompactThreads);
+    s_off[k] = e1;
+  }
+  if (c0 && c0 <= 16 && e0 + c0 <= cap_vals)
+    sparse_copy16(vslot + b0 * 512, reinterpret_cast<const uint4*>(masks16 + b0 * 32), vals + e0, c0);
+  if (c1 && c1 <= 16 && e1 + c1 <= cap_vals)
+    sparse_copy16(vslot + b1 * 512, reinterpret_cast<const uint4*>(masks16 + b1 * 32), vals + e1, c1);
   __syncthreads();
   // dense blocks: lane l owns the block's coefficients 16 l .. 16 l + 15 (mask word l),
   // so the slot reads and the packed writes of a warp are both contiguous
   const uint32_t nd = s_ndense;
-  for (uint32_t i = warp; i < nd; i += kCompactThreads / 32) {
+  for (uint32_t i = warp; i < nd; i += NW) {
     const uint64_t bb = (uint64_t)chunk * kOffChunk + s_dense[i];
     const uint32_t m = masks16[bb * 32 + lane];
     uint32_t kept;
     const uint32_t off = warp_exscan_small((uint32_t)__popc(m), lane, kept);
     const double* src = vslot + bb * 512 + lane;
     double* dst = vals + s_off[i] + off;
+    double v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = ((m >> r) & 1u) ? __ldcs(src + 32 * r) : 0.0;
     int k = 0;
 #pragma unroll
-    for (int h = 0; h < 16; h += 4) {  // four loads in flight, then their stores
-      double v[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) v[r] = ((m >> (h + r)) & 1u) ? __ldcs(src + 32 * (h + r)) : 0.0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if ((m >> (h + r)) & 1u) dst[k++] = v[r];
-    }
+    for (int r = 0; r < 16; ++r)
+      if ((m >> r) & 1u) dst[k++] = v[r];
   }
 }
 
