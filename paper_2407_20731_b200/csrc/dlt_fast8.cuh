@@ -68,16 +68,16 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t x) {
 }
 // exclusive prefix of per-lane counts v <= 31 without a dependent shuffle chain:
 // five independent ballots over the bits of v
+// (the total by one REDUX: callers that only need it drop the ballots entirely)
 __device__ __forceinline__ uint32_t warp_exscan_small(uint32_t v, int lane, uint32_t& total) {
   const uint32_t lt = (1u << lane) - 1u;
-  uint32_t pre = 0, tot = 0;
+  uint32_t pre = 0;
 #pragma unroll
   for (int b = 0; b < 5; ++b) {
     const uint32_t bal = __ballot_sync(0xffffffffu, (v >> b) & 1u);
     pre += (uint32_t)__popc(bal & lt) << b;
-    tot += (uint32_t)__popc(bal) << b;
   }
-  total = tot;
+  total = __reduce_add_sync(0xffffffffu, v);
   return pre;
 }
 __device__ __forceinline__ uint32_t warp_exscan_u32(uint32_t v, int lane) {
@@ -1441,10 +1441,14 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
         const uint32_t bse = __shfl_sync(0xffffffffu, inoff, ml);
         const uint32_t lb = (lky & 1) ? 8u : 0u;
         double a8[8];
+        // running offset over this line's four mask bits (one popcount for the low half)
+        const uint32_t mh = mw >> lb;
+        const double* sl = sv0 + bse + (lb ? (uint32_t)__popc(mw & 0xffu) : 0u);
 #pragma unroll
         for (int kx = 0; kx < 4; ++kx) {
-          const uint32_t bit = lb + kx;
-          a8[kx] = ((mw >> bit) & 1u) ? sv0[bse + __popc(mw & ((1u << bit) - 1u))] : 0.0;
+          const uint32_t b = (mh >> kx) & 1u;
+          a8[kx] = b ? *sl : 0.0;
+          sl += b;
         }
         inv1_low8<1, 0, 0>(a8);  // inverse x sweep
         __syncwarp();            // the values region is read: reuse the stage
