@@ -696,31 +696,77 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
 }
 
 // Generic compress epilogue: pack the slots (natural index, N3 doubles per block) into
-// the value region.  One warp per block, one 64-bit mask word at a time: lane l moves
-// the word's bits 2l and 2l + 1 (rank = popcount of the lower bits), so reads and
-// writes stay contiguous for dense blocks and all-zero words cost one test.
+// the value region.  One warp per block: the block's mask words (lane l holds words l
+// and l + 32) and its offsets arrive in one round of loads and their prefix counts by
+// a warp scan; then the non-empty words are walked four at a time with every value
+// load of a group in flight before its stores (lane l moves bits 2l and 2l + 1 of each word, so
+// reads and writes stay contiguous for dense blocks).  The earlier loop loaded one mask
+// word, then its values, then stored, word after word: ~2 W dependent round trips per
+// block.
 __global__ void __launch_bounds__(256) compact_generic_kernel(const uint8_t* stream, uint64_t nblocks,
                                                             uint64_t mask_off, int W, int N3, const uint64_t* off,
-                                                            const double* vslot, double* vals, uint64_t cap_vals,
+                                                            const double* __restrict__ vslot,
+                                                            double* __restrict__ vals, uint64_t cap_vals,
                                                             unsigned long long* flags) {
   const int lane = threadIdx.x & 31;
   const uint64_t* masks = reinterpret_cast<const uint64_t*>(stream + mask_off);
   const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const int p2 = 2 * lane;  // this lane's two bits of every 64-bit mask word
+  const uint64_t lowm = (1ull << p2) - 1ull;
   for (uint64_t b = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nblocks; b += nw) {
-    const uint64_t e = off[b], cnt = off[b + 1] - e;
+    const uint64_t e = off[b], e1 = off[b + 1];
+    const uint64_t m0 = lane < W ? masks[b * W + lane] : 0ull;
+    const uint64_t m1 = lane + 32 < W ? masks[b * W + lane + 32] : 0ull;
+    const uint64_t cnt = e1 - e;
     if (b + 1 == nblocks && lane == 0 && off[nblocks] > cap_vals) atomicOr(flags, kFlagOverflow);
     if (cnt == 0 || e + cnt > cap_vals) continue;  // warp-uniform
+    // exclusive prefix of the words' popcounts (words 0..31, then 32..63)
+    const uint32_t c0 = (uint32_t)__popcll(m0), c1 = (uint32_t)__popcll(m1);
+    uint32_t x0 = c0, x1 = c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t0 = __shfl_up_sync(0xffffffffu, x0, o), t1 = __shfl_up_sync(0xffffffffu, x1, o);
+      if (lane >= o) {
+        x0 += t0;
+        x1 += t1;
+      }
+    }
+    const uint32_t tot0 = __shfl_sync(0xffffffffu, x0, 31);
+    x0 -= c0;
+    x1 += tot0 - c1;
     const double* src = vslot + b * (uint64_t)N3;
-    uint64_t base = e;
-    const int p2 = 2 * lane;  // this lane's two bits of every 64-bit mask word
-    for (int w = 0; w < W; ++w) {
-      const uint64_t m = masks[b * W + w];  // same word for the whole warp
-      if (m == 0) continue;
-      const uint32_t r0 = (uint32_t)__popcll(m & ((1ull << p2) - 1ull));
-      const uint32_t b0 = (uint32_t)(m >> p2) & 1u, b1 = (uint32_t)(m >> (p2 + 1)) & 1u;
-      if (b0) vals[base + r0] = __ldcs(src + 64 * w + p2);
-      if (b1) vals[base + r0 + b0] = __ldcs(src + 64 * w + p2 + 1);
-      base += (uint32_t)__popcll(m);
+    double* dst = vals + e;
+    // non-empty words only, four at a time (warp-uniform word indices)
+    uint64_t nz = (uint64_t)__ballot_sync(0xffffffffu, m0 != 0ull) |
+                  ((uint64_t)__ballot_sync(0xffffffffu, m1 != 0ull) << 32);
+    while (nz) {
+      uint64_t m[4];
+      uint32_t wb[4];
+      int wi[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int w = nz ? __ffsll((long long)nz) - 1 : 0;
+        const bool live = nz != 0ull;
+        nz &= nz - 1;
+        const uint64_t a = __shfl_sync(0xffffffffu, m0, w & 31), c = __shfl_sync(0xffffffffu, m1, w & 31);
+        const uint32_t ba = __shfl_sync(0xffffffffu, x0, w & 31), bc = __shfl_sync(0xffffffffu, x1, w & 31);
+        m[q] = live ? (w < 32 ? a : c) : 0ull;
+        wb[q] = w < 32 ? ba : bc;
+        wi[q] = w;
+      }
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v[2 * q] = ((m[q] >> p2) & 1ull) ? __ldcs(src + 64 * wi[q] + p2) : 0.0;
+        v[2 * q + 1] = ((m[q] >> (p2 + 1)) & 1ull) ? __ldcs(src + 64 * wi[q] + p2 + 1) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t r0 = wb[q] + (uint32_t)__popcll(m[q] & lowm);
+        const uint32_t b0 = (uint32_t)(m[q] >> p2) & 1u;
+        if (b0) dst[r0] = v[2 * q];
+        if ((m[q] >> (p2 + 1)) & 1ull) dst[r0 + b0] = v[2 * q + 1];
+      }
     }
   }
 }
