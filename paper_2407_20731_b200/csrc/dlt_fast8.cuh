@@ -320,9 +320,13 @@ __device__ __noinline__ bool select_bins16(uint32_t tpark, int lane, uint64_t R,
   __syncwarp();
   uint64_t key = lane < (int)ncand ? cand[lane] : ~0ull;
   __syncwarp();
-  // bitonic sort of the 32 keys, ascending by lane
+  // bitonic sort ascending by lane of the first NS keys, NS the power of two >= ncand
+  // (warp-uniform): partners stay inside NS-lane groups and the lanes past ncand hold
+  // the largest key, so the live lanes end sorted exactly as with all 32
+  const int NS = ncand <= 2 ? 2 : ncand <= 4 ? 4 : ncand <= 8 ? 8 : ncand <= 16 ? 16 : 32;
 #pragma unroll
-  for (int k = 2; k <= 32; k <<= 1)
+  for (int k = 2; k <= 32; k <<= 1) {
+    if (k > NS) break;
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
       const uint64_t o = __shfl_xor_sync(0xffffffffu, key, j);
@@ -330,6 +334,7 @@ __device__ __noinline__ bool select_bins16(uint32_t tpark, int lane, uint64_t R,
       const bool lower = ((lane & j) == 0);
       key = (lower == up) ? (o < key ? o : key) : (o > key ? o : key);
     }
+  }
   const uint64_t h = lane < (int)ncand ? hi_v2(__longlong_as_double((long long)key), f, sB) : 0ull;
   uint64_t cs = h;
 #pragma unroll

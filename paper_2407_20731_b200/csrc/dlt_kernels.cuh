@@ -450,8 +450,13 @@ __device__ __noinline__ void select_bin(const double* u, uint64_t mb, uint64_t e
       if (ncd <= 32) {
         uint64_t key = lane < (int)ncd ? ckey[lane] : ~0ull;
         uint32_t kix = lane < (int)ncd ? cix[lane] : 0xffffffffu;
+        // bitonic sort by key (the index rides along) of the first NS lanes only, NS the
+        // power of two >= ncd (warp-uniform): partners stay inside NS-lane groups and the
+        // lanes past ncd hold the largest key, so the live lanes end sorted as with 32
+        const int NS = ncd <= 2 ? 2 : ncd <= 4 ? 4 : ncd <= 8 ? 8 : ncd <= 16 ? 16 : 32;
 #pragma unroll
-        for (int kb = 2; kb <= 32; kb <<= 1)  // bitonic sort by key (the index rides along)
+        for (int kb = 2; kb <= 32; kb <<= 1) {
+          if (kb > NS) break;
 #pragma unroll
           for (int j = kb >> 1; j > 0; j >>= 1) {
             const uint64_t o = __shfl_xor_sync(0xffffffffu, key, j);
@@ -460,6 +465,7 @@ __device__ __noinline__ void select_bin(const double* u, uint64_t mb, uint64_t e
             const bool sw = (lower == up) ? (o < key) : (o > key);
             if (sw) { key = o; kix = oi; }
           }
+        }
         const bool live = lane < (int)ncd;
         const uint64_t hv =
             live ? (uint64_t)__double_as_longlong(tB(__longlong_as_double((long long)key))) - C52 + 1ull : 0ull;
