@@ -601,6 +601,18 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
   uint32_t next = 0;
   if (lane == 0) next = atomicAdd(A.ws.counter, 1u);
   next = __shfl_sync(0xffffffffu, next, 0);
+  // small scalar RelativeL2 blocks (lx <= 7): the next block's values are loaded into
+  // registers while this one is transformed and selected (ceil(lx^3 / 32) doubles per
+  // lane), so the block loop does not wait on DRAM at its start
+  constexpr bool kPf = LX <= 7;
+  constexpr int NPF = kPf ? (N3 + 31) / 32 : 1;
+  const bool pf_on = kPf && A.comps == 1 && !A.norm;
+  double pf[NPF];
+  if (pf_on && next < A.ws.ntiles) {
+    const double* s0 = A.field + (uint64_t)next * N3;
+#pragma unroll
+    for (int i = 0; i < NPF; ++i) pf[i] = (tid + 32 * i < N3) ? s0[tid + 32 * i] : 0.0;
+  }
   for (;;) {
     const uint32_t tile = next;
     if (tile >= A.ws.ntiles) {
@@ -615,7 +627,11 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
     uint64_t um = 0;
     // scalar field, RelativeL2: plain contiguous copy, 4 loads in flight (lx <= 10;
     // at lx = 12 this variant measured 7 % slower, so it keeps the general loop)
-    if (LX <= 10 && A.comps == 1 && !A.norm) {
+    if (pf_on) {
+#pragma unroll
+      for (int i = 0; i < NPF; ++i)
+        if (tid + 32 * i < N3) u[tid + 32 * i] = pf[i];
+    } else if (LX <= 10 && A.comps == 1 && !A.norm) {
 #pragma unroll 4
       for (int p = tid; p < N3; p += kGenCThreads) u[p] = src[p];
     } else {  // (also for RelativeL2 at lx > 10: a loop without the maximum measured 8-10 % slower)
@@ -640,6 +656,14 @@ __global__ void __launch_bounds__(kGenCThreads) compress_generic(CompressArgs A)
     for (int l = tid; l < N2; l += kGenCThreads) {
       const uint64_t m = fwd_line_ptr_mb<LX>(u + l * N, 1);  // x
       mbl = m > mbl ? m : mbl;
+    }
+    if (pf_on) {  // the next block's values (its ticket is back by now)
+      const uint32_t nt = __shfl_sync(0xffffffffu, next, 0);
+      if (nt < A.ws.ntiles) {
+        const double* s0 = A.field + (uint64_t)nt * N3;
+#pragma unroll
+        for (int i = 0; i < NPF; ++i) pf[i] = (tid + 32 * i < N3) ? s0[tid + 32 * i] : 0.0;
+      }
     }
     __syncthreads();
     if (kGenCThreads == 32 || warp == 0) {  // single-warp CTA: no divergent region
