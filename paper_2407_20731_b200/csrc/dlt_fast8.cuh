@@ -516,13 +516,16 @@ __device__ __forceinline__ Sel16 select16(double (&v)[16], int lane, uint64_t ep
       tm = tb > tm ? tb : tm;
     }
     const uint64_t gtm = warp_max_u64(tm);
+    // t >= 2^52 > 0 and finite: double equality == bit-pattern equality, one DSETP per
+    // candidate test instead of the two-word integer compare
+    const double gtmd = __longlong_as_double((long long)gtm);
     // every remaining move removes at most this hi: give up early (exactly) when the
     // moves left cannot cover the excess (turbulent spectra need hundreds of moves)
     if (SNc - thr > (uint64_t)(kMaxMoves - mv) * (gtm - C52 + 1ull)) break;
     uint32_t cm = 0;
 #pragma unroll
     for (int r = 0; r < 16; ++r)
-      if (!((mK >> r) & 1u) && (uint64_t)__double_as_longlong(t[r]) == gtm) cm |= 1u << r;
+      if (!((mK >> r) & 1u) && t[r] == gtmd) cm |= 1u << r;
     const uint32_t ncand = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(cm));
     if (ncand == 0) break;  // defensive (cannot happen while SNc > thr)
     uint32_t gidx;
