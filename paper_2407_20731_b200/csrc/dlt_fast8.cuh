@@ -1307,6 +1307,12 @@ __host__ __device__ constexpr int d8_smem() { return d8_warps<ERR>() * kD8WarpBy
 // round, reconstructed into a shared-memory copy of those elements (point-major,
 // component-minor) and written out with coalesced 128-bit stores (12 warps with a
 // double buffer and one barrier per round measured 7 % slower: fewer warps)
+// plain scalar decode: each block's reconstruction leaves through one TMA bulk store
+// (evict-first) from the stage instead of eight 128-bit streaming stores per lane
+// (decompress 5.95 -> 6.06 TB/s, profiles/r2_summary.md)
+#ifndef ISF_D8_TMASTORE
+#define ISF_D8_TMASTORE 1
+#endif
 #ifndef ISF_D8V_WARPS
 #define ISF_D8V_WARPS 15
 #endif
@@ -1359,6 +1365,7 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
   __syncwarp();
   pdl_wait();
   pdl_launch_dependents();
+  const uint64_t pol_out = ISF_D8_TMASTORE ? l2_policy_evict_first() : 0ull;  // TS: the output is streamed
   // the TMA stage only carries the block's value range; offsets (from the counts) and
   // the lane's 16-bit mask word travel in registers, loaded two blocks ahead
   auto issue = [&](uint64_t blk, int st, uint64_t o0, uint64_t o1) {
@@ -1552,16 +1559,39 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
         v[2 * z + 1] = t.y;
       }
     }
-    fence_proxy_async();
-    __syncwarp();
-    issue(blk + 2 * W, st, r0, r1);
+    // TS (scalar plain decode): the stage also carries the reconstruction out through
+    // one TMA bulk store, so its refill waits for that store's read
+    constexpr bool TS = ISF_D8_TMASTORE && !ERR && !VEC;
+    const int st_cur = st;
+    if constexpr (!TS) {
+      fence_proxy_async();
+      __syncwarp();
+      issue(blk + 2 * W, st, r0, r1);
+    }
     st ^= 1;
     o0 = p0; o1 = p1;
+    const uint64_t rr0 = r0, rr1 = r1;
     p0 = r0; p1 = r1;
     mc = mn; mn = mr;
     if (lowz) inv2_low8<2, 0, 1, 2>(v); else lines8<2, 2, 0, 1, 2, true>(v);  // inverse z sweep
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = __dadd_rn(v[r], 0.0);  // zeros as +0
+    if constexpr (TS) {
+      double2* so = reinterpret_cast<double2*>(wbase + st_cur * kD8StageBytes);
+      __syncwarp();  // every lane's z-line loads of the stage are done
+#pragma unroll
+      for (int z = 0; z < 8; ++z) so[z * 32 + lane] = make_double2(v[2 * z], v[2 * z + 1]);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_s2g_hint(A.out + blk * 512, so, 4096u, pol_out);
+        bulk_commit();
+      }
+      // the stage is read: refill it (waiting here measured faster than deferring the
+      // wait and the refill to the next block's start: 6.06 vs 6.00 TB/s)
+      if (lane == 0) bulk_wait_read0();
+      issue(blk + 2 * W, st_cur, rr0, rr1);
+    }
     // vector field (the block is every third double of its element): VEC stages the
     // CTA's elements in shared memory; the error-report instantiation stores strided
     const bool vec = ERR && A.comps == 3;
@@ -1586,7 +1616,7 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
         dv[192 * z] = v[2 * z];
         dv[192 * z + 3] = v[2 * z + 1];
       }
-    } else {
+    } else if (!ISF_D8_TMASTORE || ERR) {
       double2* dst = reinterpret_cast<double2*>(A.out + blk * 512) + lane;
 #pragma unroll
       for (int z = 0; z < 8; ++z) stg_stream(dst + z * 32, make_double2(v[2 * z], v[2 * z + 1]));
@@ -1677,6 +1707,9 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
     if (warp % 3 == 0 && lane == 0) bulk_wait0();  // the element stores are complete
   }
 #endif
+  if constexpr (ISF_D8_TMASTORE && !ERR && !VEC) {
+    if (lane == 0) bulk_wait0();  // the block stores are complete
+  }
   __shared__ double s_red[4 * kNW];
   if (last_cta(A.ws.counter + 1)) finalize_cta(P.fin, s_red);
 }
