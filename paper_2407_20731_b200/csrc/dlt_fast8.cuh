@@ -26,8 +26,8 @@ namespace dev {
 #ifndef ISF_C8_WARPS
 #define ISF_C8_WARPS 16
 #endif
-#ifndef ISF_D8_WARPS
-#define ISF_D8_WARPS 24
+#ifndef ISF_D8_WARPS  // decompress8 warps per CTA (profiles/r2_summary.md, with the TMA block store:
+#define ISF_D8_WARPS 20  // 16 / 18 / 20 / 21 / 22 / 24 -> 5.99 / 5.73 / 6.25 / 5.62 / 5.66 / 6.07 TB/s on TGV)
 #endif
 #ifndef ISF_D8E_WARPS
 #define ISF_D8E_WARPS 16
