@@ -1662,7 +1662,8 @@ __global__ void __launch_bounds__((VEC ? kD8VecWarps : d8_warps<ERR>()) * 32) de
       asm volatile("bar.sync %0, 96;" ::"r"(1u + le) : "memory");
       if (warp % 3 == 0 && lane == 0) {
         if (e < B / 3) {
-          bulk_s2g(A.out + e * 1536, obuf + ((kD8VecBufs == 2 ? (it & 1) * kD8VecElems : 0) + le) * 1536, 1536 * 8);
+          bulk_s2g_hint(A.out + e * 1536, obuf + ((kD8VecBufs == 2 ? (it & 1) * kD8VecElems : 0) + le) * 1536, 1536 * 8,
+                        pol_out);  // streamed like the scalar path's block stores
           bulk_commit();
         }
         if constexpr (kD8VecBufs == 1) {
